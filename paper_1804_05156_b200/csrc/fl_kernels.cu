@@ -1,0 +1,905 @@
+// fl_kernels.cu -- device side of the B200 P1 assembly path (v1, general).
+//
+// Pipeline:
+//   plan    k_inc_count -> scan -> k_inc_fill -> k_inc_sort -> k_plan_stats
+//           node -> incidence lists sorted by (local index j, element t): the
+//           order in which the reference's blockwise triplets reach a column
+//           (assembly.hpp:486-498 + the stable counting sorts sparse.hpp:79-89).
+//   mark    k_mark_boundary -> scan -> k_partition (partition_boundary, system.hpp:50-67)
+//   column  k_columns<D>: one warp per output column c = one reference CSC column,
+//           exact per-entry summation order (i, j, t), zero drop, fused load
+//           vector, Neumann, Dirichlet lift, A(free,free) and b_f, with CSC
+//           offsets from a decoupled look-back over column tiles.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "fl_geometry.cuh"
+#include "fl_internal.cuh"
+#include "fl_kernels.cuh"
+#include "fl_scan.cuh"
+
+namespace fl {
+
+// ===========================================================================
+// plan
+// ===========================================================================
+__global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ elems,
+                            int32_t* __restrict__ cnt, uint32_t* __restrict__ err) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(elems + e);
+        if (v < 0 || v >= n_nodes) {
+            atomicOr(err, DERR_INDEX);
+            continue;
+        }
+        atomicAdd(cnt + v, 1);
+    }
+}
+
+__global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes,
+                           const int32_t* __restrict__ elems, const int32_t* __restrict__ inc_ptr,
+                           int32_t* __restrict__ cursor, uint32_t* __restrict__ inc) {
+    const int64_t n_entries = (int64_t)n_elems * nv;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(elems + e);
+        if (v < 0 || v >= n_nodes) continue;
+        const int32_t t = (int32_t)(e / nv);
+        const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
+        const int32_t pos = __ldg(inc_ptr + v) + atomicAdd(cursor + v, 1);
+        inc[pos] = (j << 30) | (uint32_t)t;
+    }
+}
+
+// Sort each node's incidence keys ascending = (j, t) order.  Segments are
+// short (2-D ~6, 3-D Kuhn 24): insertion sort per thread.
+__global__ void k_inc_sort(int32_t n_nodes, const int32_t* __restrict__ inc_ptr,
+                           uint32_t* __restrict__ inc) {
+    const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_nodes) return;
+    const int32_t p0 = inc_ptr[c], p1 = inc_ptr[c + 1];
+    for (int32_t a = p0 + 1; a < p1; ++a) {
+        const uint32_t key = inc[a];
+        int32_t b = a - 1;
+        while (b >= p0 && inc[b] > key) {
+            inc[b + 1] = inc[b];
+            --b;
+        }
+        inc[b + 1] = key;
+    }
+}
+
+// stats[0] += sum_c min(m_c * d + 1, N)  (nnz upper bound), stats[1] = max m_c
+__global__ void k_plan_stats(int32_t n_nodes, int dim, const int32_t* __restrict__ inc_ptr,
+                             unsigned long long* __restrict__ stats) {
+    int64_t bound = 0;
+    int32_t mx = 0;
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_nodes;
+         c += gridDim.x * blockDim.x) {
+        const int32_t m = inc_ptr[c + 1] - inc_ptr[c];
+        const int64_t b = (int64_t)m * dim + 1;
+        bound += b < n_nodes ? b : n_nodes;
+        mx = m > mx ? m : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bound += __shfl_xor_sync(0xffffffffu, bound, o);
+        const int32_t y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(stats, (unsigned long long)bound);
+        atomicMax(stats + 1, (unsigned long long)mx);
+    }
+}
+
+// ===========================================================================
+// validation (make_mesh, mesh.hpp:187-226)
+// ===========================================================================
+template <int D>
+__global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __restrict__ nodes,
+                           const int32_t* __restrict__ elems, const int8_t* __restrict__ flags,
+                           uint32_t* __restrict__ err) {
+    constexpr int NV = D + 1;
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_elems;
+         t += gridDim.x * blockDim.x) {
+        int32_t v[NV];
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            v[k] = elems[(size_t)t * NV + k];
+            ok &= (v[k] >= 0 && v[k] < n_nodes);
+            if (flags) {
+                const int8_t f = flags[(size_t)t * NV + k];
+                if (f < 0 || f > 3) atomicOr(err, DERR_FLAG);
+            }
+        }
+        if (!ok) {
+            atomicOr(err, DERR_INDEX);
+            continue;
+        }
+        double m;
+        if (D == 2) {
+            const double* a = nodes + 2 * (size_t)v[0];
+            const double* b = nodes + 2 * (size_t)v[1];
+            const double* c = nodes + 2 * (size_t)v[2];
+            // mesh.hpp:73-77
+            const double e2x = a[0] - c[0], e2y = a[1] - c[1];
+            const double e3x = b[0] - a[0], e3y = b[1] - a[1];
+            m = 0.5 * (-e3x * e2y + e3y * e2x);
+        } else {
+            const double* p1 = nodes + 3 * (size_t)v[0];
+            const double* p2 = nodes + 3 * (size_t)v[1];
+            const double* p3 = nodes + 3 * (size_t)v[2];
+            const double* p4 = nodes + 3 * (size_t)v[NV - 1];
+            // mesh.hpp:81-90 (division by 6 keeps the sign: test the numerator)
+            const double ax = p2[0] - p1[0], ay = p2[1] - p1[1], az = p2[2] - p1[2];
+            const double bx = p3[0] - p1[0], by = p3[1] - p1[1], bz = p3[2] - p1[2];
+            const double cx = p4[0] - p1[0], cy = p4[1] - p1[1], cz = p4[2] - p1[2];
+            const double nx = ay * bz - az * by;
+            const double ny = az * bx - ax * bz;
+            const double nz = ax * by - ay * bx;
+            m = (nx * cx + ny * cy + nz * cz) / 6.0;
+        }
+        if (!(m > 0.0)) atomicOr(err, DERR_MEASURE);
+    }
+}
+
+// ===========================================================================
+// boundary marking: partition_boundary (system.hpp:50-67) / boundary_faces
+// (mesh.hpp:261-285).  is_dir[v] = 1 for every vertex of a flag-1 face.
+// ===========================================================================
+template <int D>
+__global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ elems,
+                                const int8_t* __restrict__ flags, int8_t* __restrict__ is_dir,
+                                int8_t* __restrict__ is_neu, uint32_t* __restrict__ counters) {
+    constexpr int NV = D + 1;
+    const int64_t n_entries = (int64_t)n_elems * NV;
+    uint32_t dir_faces = 0, neu_faces = 0, err = 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t f = flags[e];
+        if (f == 0) continue;
+        if (f == 3) err |= DERR_ROBIN;
+        if (f < 0 || f > 3) err |= DERR_FLAG;
+        if (f != 1 && f != 2) continue;
+        const int32_t t = (int32_t)(e / NV);
+        const int lf = (int)(e - (int64_t)t * NV);
+        int8_t* mark = (f == 1) ? is_dir : is_neu;
+        if (f == 1) ++dir_faces;
+        else ++neu_faces;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (k != lf) mark[elems[(size_t)t * NV + k]] = 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dir_faces += __shfl_xor_sync(0xffffffffu, dir_faces, o);
+        neu_faces += __shfl_xor_sync(0xffffffffu, neu_faces, o);
+        err |= __shfl_xor_sync(0xffffffffu, err, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (dir_faces) atomicAdd(counters + CNT_DIR_FACES, dir_faces);
+        if (neu_faces) atomicAdd(counters + CNT_NEU_FACES, neu_faces);
+        if (err) atomicOr(counters + CNT_ERR, err);
+    }
+}
+
+// free rank scan output -> lists (ascending, system.hpp:63-65) and row map
+__global__ void k_partition(int32_t n_nodes, const int8_t* __restrict__ is_dir,
+                            const int32_t* __restrict__ free_rank, int32_t* __restrict__ fidx,
+                            int32_t* __restrict__ dir_nodes, int32_t* __restrict__ free_nodes,
+                            uint32_t* __restrict__ counters) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_nodes;
+         k += gridDim.x * blockDim.x) {
+        const int32_t fr = free_rank[k];
+        if (is_dir[k]) {
+            fidx[k] = -1;
+            dir_nodes[k - fr] = k;
+        } else {
+            fidx[k] = fr;
+            free_nodes[fr] = k;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) counters[CNT_N_DIR] = n_nodes - free_rank[n_nodes];
+}
+
+// ===========================================================================
+// column kernel
+// ===========================================================================
+constexpr int kHS = 256;           // per-warp slot table (distinct rows of a column)
+constexpr int kMaxSlots = 192;     // load factor 0.75
+constexpr int kMaxNeu = 128;       // Neumann items per node
+constexpr int kWarps = 4;          // columns per tile (one warp each)
+constexpr int32_t kEmpty = -1;
+
+struct WarpSmem {
+    int32_t keys[kHS];
+    double acc[kHS];
+    double tacc[kHS];
+    int32_t out_rows[kHS];
+    double out_vals[kHS];
+    int32_t ff_rows[kHS];
+    double ff_vals[kHS];
+    double stage[32];
+    uint32_t neu_key[kMaxNeu];
+    double neu_val[kMaxNeu];
+    int32_t n_a, n_ff;
+};
+
+__device__ __forceinline__ uint32_t slot_hash(int32_t row) {
+    return ((uint32_t)row * 2654435761u) >> 24;  // 8 bits
+}
+
+__device__ __forceinline__ int find_or_insert(WarpSmem& ws, int32_t row) {
+    uint32_t h = slot_hash(row);
+    while (true) {
+        const int32_t prev = atomicCAS(&ws.keys[h], kEmpty, row);
+        if (prev == kEmpty) {
+            ws.acc[h] = -0.0;   // -0.0 + x == x for every x: the fold starts at
+            ws.tacc[h] = -0.0;  // the first value exactly as sparse.hpp:101
+            return (int)h;
+        }
+        if (prev == row) return (int)h;
+        h = (h + 1) & (kHS - 1);
+    }
+}
+
+__device__ __forceinline__ int find_slot(const WarpSmem& ws, int32_t row) {
+    uint32_t h = slot_hash(row);
+    while (ws.keys[h] != row) h = (h + 1) & (kHS - 1);
+    return (int)h;
+}
+
+__device__ __forceinline__ double field_at_node(const FieldDesc& g, const double* nodes, int dim,
+                                                int32_t k) {
+    if (g.kind == FL_FIELD_SAMPLES) return __ldg(g.samples + k);
+    if (g.kind == FL_FIELD_CONST) return g.value;
+    const double x = nodes[(size_t)k * dim];
+    const double y = nodes[(size_t)k * dim + 1];
+    const double z = dim == 3 ? nodes[(size_t)k * dim + 2] : 0.0;
+    return eval_point(g, x, y, z);
+}
+
+// Bitonic sort of up to kHS (row, val, tval) entries in warp smem, ascending row.
+__device__ void smem_sort_rows(int32_t* rows, double* vals, int n, int lane) {
+    int p2 = 1;
+    while (p2 < n) p2 <<= 1;
+    for (int i = n + lane; i < p2; i += 32) rows[i] = INT_MAX;
+    __syncwarp();
+    for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < p2; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    if ((rows[i] > rows[ixj]) == up) {
+                        const int32_t r = rows[i];
+                        rows[i] = rows[ixj];
+                        rows[ixj] = r;
+                        const double v = vals[i];
+                        vals[i] = vals[ixj];
+                        vals[ixj] = v;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int D>
+struct Lane {
+    int32_t t;
+    int j;
+    bool valid;
+    int32_t R[D + 1];
+    double s[D + 1];
+    double l;
+};
+
+template <int D>
+__device__ __forceinline__ void lane_compute(const ColParams& p, Lane<D>& L, int32_t p0, int32_t m,
+                                             int k, const Recip& R3, const Recip& R6,
+                                             ElemCol<D>& ec) {
+    L.valid = k < m;
+    if (!L.valid) return;
+    const uint32_t key = __ldg(p.inc + p0 + k);
+    L.t = (int32_t)(key & 0x3FFFFFFFu);
+    L.j = (int)(key >> 30);
+    if (D == 3) {
+        const int4 q = __ldg(reinterpret_cast<const int4*>(p.elems) + L.t);
+        L.R[0] = q.x;
+        L.R[1] = q.y;
+        L.R[2] = q.z;
+        L.R[D] = q.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i <= D; ++i) L.R[i] = __ldg(p.elems + (size_t)L.t * (D + 1) + i);
+    }
+    ec.load(p.nodes, L.R);
+    double meas;
+    if constexpr (D == 2) meas = ec.stiffness_col(L.j, L.s);
+    else meas = ec.stiffness_col(L.j, L.s, R6);
+    if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
+    if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
+        double a;
+        if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
+        else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + L.t);
+        else a = ec.coef_c5(R3);
+#pragma unroll
+        for (int i = 0; i <= D; ++i) L.s[i] = L.s[i] * a;
+    }
+    if (p.want_b) {
+        if constexpr (D == 2) L.l = ec.load_col(L.j, L.t, p.f, R6);
+        else L.l = ec.load_col(L.j, L.t, meas, p.f);
+    } else {
+        L.l = 0.0;
+    }
+}
+
+// One warp assembles column c.  Results stay in ws (out_* lists) until the
+// tile offsets are known.
+template <int D>
+__device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lane,
+                            double& b_out, double& bmod_out, double& u0_out) {
+    const unsigned FULL = 0xffffffffu;
+    const int32_t p0 = p.inc_ptr[c];
+    const int32_t m = p.inc_ptr[c + 1] - p0;
+    const int nchunks = (m + 31) >> 5;
+    const Recip R3 = recip(3.0);
+    const Recip R6 = recip(6.0);
+
+    for (int h = lane; h < kHS; h += 32) ws.keys[h] = kEmpty;
+    const int w = threadIdx.x >> 5;
+    if (lane == 0) ws.n_a = ws.n_ff = 0;
+    __syncwarp();
+
+    if ((int64_t)m * D + 1 > kMaxSlots && p.want_a) {
+        if (lane == 0) atomicOr(p.err, DERR_OVERFLOW);
+        b_out = bmod_out = u0_out = 0.0;
+        return;
+    }
+
+    Lane<D> L;
+    ElemCol<D> ec;
+    double b = 0.0;
+    // ---- normal passes: order (i, k) == the reference's (i*(d+1)+j, t) per entry
+    for (int i = 0; i <= D; ++i) {
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (i == 0 || nchunks > 1) {
+                lane_compute<D>(p, L, p0 + ch * 32, m - ch * 32, lane, R3, R6, ec);
+                if (i == 0 && p.want_b) {
+                    // b[c] = 0.0 + contributions in (j, t) order (system.hpp:114-118)
+                    const int cnt = min(32, m - ch * 32);
+                    for (int q = 0; q < cnt; ++q) b = b + __shfl_sync(FULL, L.l, q);
+                }
+            }
+            if (!p.want_a) continue;
+            const int32_t key = L.valid ? L.R[i] : kEmpty;
+            const unsigned g = __match_any_sync(FULL, key);
+            ws.stage[lane] = L.s[i];
+            __syncwarp();
+            if (L.valid && lane == __ffs(g) - 1) {
+                const int slot = find_or_insert(ws, key);
+                double a = ws.acc[slot];
+                for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
+                ws.acc[slot] = a;
+            }
+            __syncwarp();
+        }
+        if (!p.want_a) break;
+    }
+
+    // ---- Neumann data (system.hpp:123-172), only at nodes on a flag-2 face
+    double neu_add = 0.0;
+    bool neu_active = false;
+    if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE && p.is_neu[c]) {
+        neu_active = true;
+        __shared__ int s_nneu[kWarps];
+        if (lane == 0) s_nneu[w] = 0;
+        __syncwarp();
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (nchunks > 1 || !p.want_a)
+                lane_compute<D>(p, L, p0 + ch * 32, m - ch * 32, lane, R3, R6, ec);
+            if (L.valid) {
+                for (int lf = 0; lf <= D; ++lf) {
+                    if (lf == L.j) continue;
+                    if (p.flags[(size_t)L.t * (D + 1) + lf] != 2) continue;
+                    const int q = atomicAdd(&s_nneu[w], 1);
+                    if (q < kMaxNeu) {
+                        ws.neu_key[q] = ((uint32_t)lf << 30) | (uint32_t)L.t;
+                        ws.neu_val[q] = ec.face_share(lf, p.g_neu, R3, L.t);
+                    } else {
+                        atomicOr(p.err, DERR_OVERFLOW);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // face-major order (lf, t) (mesh.hpp:268-283), accumulate from 0.0
+            const int n = min(s_nneu[w], kMaxNeu);
+            double add = 0.0;
+            uint32_t last = 0;
+            bool first = true;
+            for (int r = 0; r < n; ++r) {
+                int best = -1;
+                for (int q = 0; q < n; ++q) {
+                    const uint32_t k2 = ws.neu_key[q];
+                    if ((first || k2 > last) && (best < 0 || k2 < ws.neu_key[best])) best = q;
+                }
+                last = ws.neu_key[best];
+                first = false;
+                add = add + ws.neu_val[best];
+            }
+            neu_add = add;
+        }
+        neu_add = __shfl_sync(FULL, neu_add, 0);
+    }
+    if (neu_active) b = b + neu_add;
+
+    // ---- transposed folds for the Dirichlet lift: A(c, r) in the order
+    //      (i_c*(d+1)+j_r, t) of entry (row c, col r) = passes (j, i, k)
+    if (p.want_a && p.need_lift) {
+        for (int jb = 0; jb <= D; ++jb)
+            for (int i = 0; i <= D; ++i)
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    if (nchunks > 1) lane_compute<D>(p, L, p0 + ch * 32, m - ch * 32, lane, R3, R6, ec);
+                    const bool act = L.valid && L.j == jb;
+                    const int32_t key = act ? L.R[i] : kEmpty;
+                    const unsigned g = __match_any_sync(FULL, key);
+                    ws.stage[lane] = L.s[i];
+                    __syncwarp();
+                    if (act && lane == __ffs(g) - 1) {
+                        const int slot = find_slot(ws, key);
+                        double a = ws.tacc[slot];
+                        for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
+                        ws.tacc[slot] = a;
+                    }
+                    __syncwarp();
+                }
+    }
+
+    // ---- compact the slot table, sort by row, drop exact zeros (sparse.hpp:105)
+    double y = 0.0;
+    if (p.want_a) {
+        __syncwarp();
+        int n = 0;
+        for (int base = 0; base < kHS; base += 32) {
+            const int h = base + lane;
+            const bool v = ws.keys[h] != kEmpty;
+            const unsigned bal = __ballot_sync(FULL, v);
+            if (v) {
+                const int pos = n + __popc(bal & ((1u << lane) - 1));
+                ws.out_rows[pos] = ws.keys[h];
+                ws.out_vals[pos] = ws.acc[h];
+            }
+            n += __popc(bal);
+        }
+        __syncwarp();
+        if (n <= 32) {
+            int32_t r = lane < n ? ws.out_rows[lane] : INT_MAX;
+            double v = lane < n ? ws.out_vals[lane] : 0.0;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    const int32_t ro = __shfl_xor_sync(FULL, r, jj);
+                    const double vo = __shfl_xor_sync(FULL, v, jj);
+                    const bool lower = (lane & jj) == 0;
+                    const bool up = (lane & k) == 0;
+                    const bool take = lower ? ((r > ro) == up) : ((r < ro) == up);
+                    if (take) {
+                        r = ro;
+                        v = vo;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < n) {
+                ws.out_rows[lane] = r;
+                ws.out_vals[lane] = v;
+            }
+            __syncwarp();
+        } else {
+            smem_sort_rows(ws.out_rows, ws.out_vals, n, lane);
+        }
+        // drop zeros (A) and restrict to free rows/cols (A_ff); keep order
+        const bool col_free = p.want_sys && p.fidx[c] >= 0;
+        int na = 0, nf = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int q = base + lane;
+            const bool in = q < n;
+            const int32_t r = in ? ws.out_rows[q] : 0;
+            const double v = in ? ws.out_vals[q] : 0.0;
+            const bool keep = in && v != 0.0;
+            const int32_t fr = (keep && col_free) ? p.fidx[r] : -1;
+            const bool keep_ff = fr >= 0;
+            const unsigned ba = __ballot_sync(FULL, keep);
+            const unsigned bf = __ballot_sync(FULL, keep_ff);
+            __syncwarp();
+            if (keep) {
+                const int pos = na + __popc(ba & ((1u << lane) - 1));
+                ws.out_rows[pos] = r;  // pos <= q: in-place forward compaction
+                ws.out_vals[pos] = v;
+            }
+            if (keep_ff) {
+                const int pos = nf + __popc(bf & ((1u << lane) - 1));
+                ws.ff_rows[pos] = fr;
+                ws.ff_vals[pos] = v;
+            }
+            na += __popc(ba);
+            nf += __popc(bf);
+            __syncwarp();
+        }
+        if (lane == 0) {
+            ws.n_a = na;
+            ws.n_ff = nf;
+        }
+        __syncwarp();
+    }
+    if (p.want_a && p.need_lift) {
+        // y = (A u0)[c]: matvec (sparse.hpp:129-141) adds A(c, r) * u0[r] over
+        // the stored entries of row c in ascending column r; A(c, r) is the
+        // transposed fold above.  Walk the slot table in ascending row order.
+        __syncwarp();
+        if (lane == 0) {
+            // gather (row, tval) from the table, then ascending-row walk
+            double yy = 0.0;
+            int32_t last = INT_MIN;
+            while (true) {
+                int32_t best = INT_MAX;
+                int bh = -1;
+                for (int h = 0; h < kHS; ++h) {
+                    const int32_t r = ws.keys[h];
+                    if (r != kEmpty && r > last && r < best) {
+                        best = r;
+                        bh = h;
+                    }
+                }
+                if (bh < 0) break;
+                last = best;
+                const double a_cr = ws.tacc[bh];
+                if (a_cr != 0.0 && p.is_dir[best]) {
+                    const double u = field_at_node(p.g_dir, p.nodes, D, best);
+                    if (u != 0.0) yy = yy + a_cr * u;
+                }
+            }
+            y = yy;
+        }
+        y = __shfl_sync(FULL, y, 0);
+    }
+
+    b_out = b;
+    double u0 = 0.0;
+    if (p.want_sys && p.is_dir[c]) u0 = field_at_node(p.g_dir, p.nodes, D, c);
+    u0_out = u0;
+    bmod_out = p.need_lift ? b - y : b - 0.0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem* wsm = reinterpret_cast<WarpSmem*>(smem_raw);
+    __shared__ int64_t s_tile;
+    __shared__ uint64_t s_off;
+    __shared__ int s_na[kWarps], s_nf[kWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpSmem& ws = wsm[w];
+
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(p.ticket, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= p.n_tiles) break;
+        const int64_t c64 = tile * kWarps + w;
+        const bool has = c64 < p.n_nodes;
+        const int32_t c = (int32_t)c64;
+        double b = 0.0, bmod = 0.0, u0 = 0.0;
+        if (has) {
+            column_warp<D>(p, c, ws, lane, b, bmod, u0);
+        } else if (lane == 0) {
+            ws.n_a = ws.n_ff = 0;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            s_na[w] = p.want_a && has ? ws.n_a : 0;
+            s_nf[w] = p.want_a && has ? ws.n_ff : 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t agg_a = 0, agg_f = 0;
+            for (int q = 0; q < kWarps; ++q) {
+                agg_a += (uint64_t)s_na[q];
+                agg_f += (uint64_t)s_nf[q];
+            }
+            // packed [61:31] = A(free,free) count, [30:0] = A count
+            s_off = lookback(p.tile_status, tile, (agg_f << 31) | agg_a);
+        }
+        __syncthreads();
+        if (has) {
+            uint64_t off_a = s_off & 0x7FFFFFFFull, off_f = s_off >> 31;
+            for (int q = 0; q < w; ++q) {
+                off_a += (uint64_t)s_na[q];
+                off_f += (uint64_t)s_nf[q];
+            }
+            if (p.want_a) {
+                const int na = s_na[w], nf = s_nf[w];
+                if ((int64_t)(off_a + na) > p.cap_a || (int64_t)(off_f + nf) > p.cap_ff) {
+                    if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
+                } else {
+                    for (int q = lane; q < na; q += 32) {
+                        p.row_idx[off_a + q] = ws.out_rows[q];
+                        p.values[off_a + q] = ws.out_vals[q];
+                    }
+                    if (lane == 0) p.col_ptr[c + 1] = (int32_t)(off_a + na);
+                    if (p.want_sys) {
+                        const int32_t fc = p.fidx[c];
+                        for (int q = lane; q < nf; q += 32) {
+                            p.ff_row_idx[off_f + q] = ws.ff_rows[q];
+                            p.ff_values[off_f + q] = ws.ff_vals[q];
+                        }
+                        if (lane == 0 && fc >= 0) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + nf);
+                    }
+                }
+            }
+            if (lane == 0) {
+                if (p.want_b) p.b[c] = b;
+                if (p.want_sys) {
+                    p.u0[c] = u0;
+                    p.b_mod[c] = bmod;
+                    const int32_t fc = p.fidx[c];
+                    if (fc >= 0) p.b_f[fc] = bmod;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t column_smem_bytes() { return sizeof(WarpSmem) * kWarps; }
+int column_tile_width() { return kWarps; }
+
+// ===========================================================================
+// general submatrix (sparse.hpp:159-183)
+// ===========================================================================
+__global__ void k_sub_rowmap(int32_t n_rows, const int32_t* __restrict__ rows,
+                             int32_t* __restrict__ row_map, int32_t bound_m,
+                             uint32_t* __restrict__ err) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_rows; q += gridDim.x * blockDim.x) {
+        const int32_t r = rows[q];
+        if (r < 0 || r >= bound_m) {
+            atomicOr(err, 1u);
+            continue;
+        }
+        if (q > 0 && r <= rows[q - 1]) atomicOr(err, 2u);
+        row_map[r] = q;
+    }
+}
+
+__global__ void k_sub_count(int32_t n_cols, const int32_t* __restrict__ cols, int32_t bound_n,
+                            const int32_t* __restrict__ col_ptr, const int32_t* __restrict__ row_idx,
+                            const int32_t* __restrict__ row_map, int32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ err) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_cols; q += gridDim.x * blockDim.x) {
+        const int32_t c = cols[q];
+        if (c < 0 || c >= bound_n) {
+            atomicOr(err, 4u);
+            cnt[q] = 0;
+            continue;
+        }
+        if (q > 0 && c <= cols[q - 1]) atomicOr(err, 8u);
+        int32_t k = 0;
+        for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) k += row_map[row_idx[e]] >= 0;
+        cnt[q] = k;
+    }
+}
+
+__global__ void k_sub_fill(int32_t n_cols, const int32_t* __restrict__ cols,
+                           const int32_t* __restrict__ col_ptr, const int32_t* __restrict__ row_idx,
+                           const double* __restrict__ values, const int32_t* __restrict__ row_map,
+                           const int32_t* __restrict__ out_ptr, int32_t* __restrict__ out_rows,
+                           double* __restrict__ out_vals) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_cols; q += gridDim.x * blockDim.x) {
+        const int32_t c = cols[q];
+        int32_t w = out_ptr[q];
+        for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+            const int32_t r = row_map[row_idx[e]];
+            if (r < 0) continue;
+            out_rows[w] = r;
+            out_vals[w] = values[e];
+            ++w;
+        }
+    }
+}
+
+// ===========================================================================
+// division self-test (fl_selftest_div)
+// ===========================================================================
+__global__ void k_selftest_div(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                               double* __restrict__ q_fast, double* __restrict__ q_ieee) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const Recip R = recip(b[i]);
+        q_fast[i] = div_by(a[i], R);
+        q_ieee[i] = __ddiv_rn(a[i], b[i]);
+    }
+}
+
+// ===========================================================================
+// host launchers
+// ===========================================================================
+int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
+    const cudaStream_t s = ctx->stream;
+    const int nv = mesh->dim + 1;
+    const int64_t n_entries = (int64_t)mesh->n_elems * nv;
+    const int32_t N = mesh->n_nodes;
+    FL_TRY(mesh->inc_ptr.ensure(sizeof(int32_t) * ((size_t)N + 1)));
+    FL_TRY(mesh->cursor.ensure(sizeof(int32_t) * ((size_t)N + 1)));
+    FL_TRY(mesh->inc.ensure(sizeof(uint32_t) * (size_t)(n_entries > 0 ? n_entries : 1)));
+    FL_TRY(mesh->stats.ensure(sizeof(unsigned long long) * 4));
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(N)));
+    int32_t* cnt = mesh->cursor.as<int32_t>();
+    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    FL_CUDA(cudaMemsetAsync(mesh->stats.p, 0, sizeof(unsigned long long) * 4, s));
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256), 1),
+                                            (int64_t)ctx->sm_count * 16);
+    if (n_entries > 0) {
+        k_inc_count<<<grid, 256, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, d_err);
+        count_launch(ctx);
+    }
+    const int32_t* cnt_c = cnt;
+    FL_CUDA(launch_scan<int32_t>(
+        N, [cnt_c] __device__(int64_t i) { return (int64_t)cnt_c[i]; },
+        mesh->inc_ptr.as<int32_t>(), ctx->scan_ws.p, s));
+    count_launch(ctx);
+    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    if (n_entries > 0) {
+        k_inc_fill<<<grid, 256, 0, s>>>(mesh->n_elems, nv, N, mesh->elems.as<int32_t>(),
+                                        mesh->inc_ptr.as<int32_t>(), cnt, mesh->inc.as<uint32_t>());
+        count_launch(ctx);
+    }
+    if (N > 0) {
+        k_inc_sort<<<div_up(N, 128), 128, 0, s>>>(N, mesh->inc_ptr.as<int32_t>(),
+                                                  mesh->inc.as<uint32_t>());
+        k_plan_stats<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            N, mesh->dim, mesh->inc_ptr.as<int32_t>(), mesh->stats.as<unsigned long long>());
+        count_launch(ctx, 2);
+    }
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+int launch_validate(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
+    if (mesh->n_elems == 0) return FL_OK;
+    const int grid = std::min(div_up(mesh->n_elems, 256), ctx->sm_count * 16);
+    const int8_t* fl = mesh->has_flags ? mesh->flags.as<int8_t>() : nullptr;
+    if (mesh->dim == 2)
+        k_validate<2><<<grid, 256, 0, ctx->stream>>>(mesh->n_elems, mesh->n_nodes,
+                                                     mesh->nodes.as<double>(),
+                                                     mesh->elems.as<int32_t>(), fl, d_err);
+    else
+        k_validate<3><<<grid, 256, 0, ctx->stream>>>(mesh->n_elems, mesh->n_nodes,
+                                                     mesh->nodes.as<double>(),
+                                                     mesh->elems.as<int32_t>(), fl, d_err);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+int launch_partition(fl_ctx* ctx, fl_mesh* mesh, fl_result* res) {
+    const cudaStream_t s = ctx->stream;
+    const int32_t N = mesh->n_nodes;
+    const int64_t n_entries = (int64_t)mesh->n_elems * (mesh->dim + 1);
+    uint32_t* counters = res->counters.as<uint32_t>();
+    int8_t* is_dir = res->is_dir.as<int8_t>();
+    int8_t* is_neu = res->is_neu.as<int8_t>();
+    FL_CUDA(cudaMemsetAsync(is_dir, 0, (size_t)N + 1, s));
+    FL_CUDA(cudaMemsetAsync(is_neu, 0, (size_t)N + 1, s));
+    if (mesh->has_flags && n_entries > 0) {
+        const int grid = (int)std::min<int64_t>(div_up(n_entries, 256), (int64_t)ctx->sm_count * 16);
+        if (mesh->dim == 2)
+            k_mark_boundary<2><<<grid, 256, 0, s>>>(mesh->n_elems, mesh->elems.as<int32_t>(),
+                                                   mesh->flags.as<int8_t>(), is_dir, is_neu, counters);
+        else
+            k_mark_boundary<3><<<grid, 256, 0, s>>>(mesh->n_elems, mesh->elems.as<int32_t>(),
+                                                   mesh->flags.as<int8_t>(), is_dir, is_neu, counters);
+        count_launch(ctx);
+    }
+    // free_rank = exclusive scan of (1 - is_dir) into the FL_B_F slot's int32 twin
+    int32_t* free_rank = res->fidx.as<int32_t>() + ((size_t)N + 1);
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(N)));
+    const int8_t* isd = is_dir;
+    FL_CUDA(launch_scan<int32_t>(
+        N, [isd] __device__(int64_t i) { return (int64_t)(isd[i] ? 0 : 1); }, free_rank,
+        ctx->scan_ws.p, s));
+    count_launch(ctx);
+    k_partition<<<std::max(1, std::min(div_up(N, 256), ctx->sm_count * 8)), 256, 0, s>>>(
+        N, is_dir, free_rank, res->fidx.as<int32_t>(), res->arr[FL_DIR_NODES].as<int32_t>(),
+        res->arr[FL_FREE_NODES].as<int32_t>(), counters);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+int launch_columns(fl_ctx* ctx, int dim, ColParams& p) {
+    const size_t smem = column_smem_bytes();
+    const int grid_max = ctx->sm_count * 4;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tiles, grid_max));
+    if (dim == 2) {
+        FL_CUDA(cudaFuncSetAttribute(k_columns<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_columns<2><<<grid, kWarps * 32, smem, ctx->stream>>>(p);
+    } else {
+        FL_CUDA(cudaFuncSetAttribute(k_columns<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        k_columns<3><<<grid, kWarps * 32, smem, ctx->stream>>>(p);
+    }
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
+                     const int32_t* row_idx, const double* values, int32_t n_rows,
+                     const int32_t* rows, int32_t n_cols, const int32_t* cols, fl_result* res,
+                     int32_t* row_map, int32_t* cnt, uint32_t* d_err, int64_t* nnz_out) {
+    const cudaStream_t s = ctx->stream;
+    FL_CUDA(cudaMemsetAsync(row_map, 0xFF, sizeof(int32_t) * ((size_t)m + 1), s));
+    if (n_rows > 0) {
+        k_sub_rowmap<<<std::max(1, std::min(div_up(n_rows, 256), ctx->sm_count * 8)), 256, 0, s>>>(
+            n_rows, rows, row_map, m, d_err);
+        count_launch(ctx);
+    }
+    if (n_cols > 0) {
+        k_sub_count<<<std::max(1, std::min(div_up(n_cols, 256), ctx->sm_count * 8)), 256, 0, s>>>(
+            n_cols, cols, n, col_ptr, row_idx, row_map, cnt, d_err);
+        count_launch(ctx);
+    }
+    FL_TRY(res->arr[FL_A_COL_PTR].ensure(sizeof(int32_t) * ((size_t)n_cols + 1)));
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(n_cols)));
+    const int32_t* cc = cnt;
+    FL_CUDA(launch_scan<int32_t>(
+        n_cols, [cc] __device__(int64_t i) { return (int64_t)cc[i]; },
+        res->arr[FL_A_COL_PTR].as<int32_t>(), ctx->scan_ws.p, s));
+    count_launch(ctx);
+    // total -> host (needed to size the outputs)
+    int32_t total = 0;
+    FL_CUDA(cudaMemcpyAsync(ctx->pinned, res->arr[FL_A_COL_PTR].as<int32_t>() + n_cols,
+                            sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    uint32_t herr = 0;
+    FL_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->pinned) + 8, d_err, sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    total = *static_cast<int32_t*>(ctx->pinned);
+    herr = *reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->pinned) + 8);
+    if (herr & (1u | 4u)) return set_error(FL_E_INDEX_OUT_OF_RANGE, "submatrix: index out of range");
+    if (herr & (2u | 8u))
+        return set_error(FL_E_UNSORTED_INDEX_SET, "submatrix: index set is not strictly increasing");
+    FL_TRY(res->arr[FL_A_ROW_IDX].ensure(sizeof(int32_t) * ((size_t)total + 1)));
+    FL_TRY(res->arr[FL_A_VALUES].ensure(sizeof(double) * ((size_t)total + 1)));
+    if (n_cols > 0) {
+        k_sub_fill<<<std::max(1, std::min(div_up(n_cols, 256), ctx->sm_count * 8)), 256, 0, s>>>(
+            n_cols, cols, col_ptr, row_idx, values, row_map, res->arr[FL_A_COL_PTR].as<int32_t>(),
+            res->arr[FL_A_ROW_IDX].as<int32_t>(), res->arr[FL_A_VALUES].as<double>());
+        count_launch(ctx);
+    }
+    FL_CUDA(cudaGetLastError());
+    *nnz_out = total;
+    return FL_OK;
+}
+
+int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
+                        double* qi) {
+    if (n <= 0) return FL_OK;
+    k_selftest_div<<<(int)std::min<int64_t>(div_up(n, 256), ctx->sm_count * 16), 256, 0,
+                     ctx->stream>>>(n, a, b, qf, qi);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+}  // namespace fl

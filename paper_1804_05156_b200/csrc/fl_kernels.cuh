@@ -1,0 +1,53 @@
+// fl_kernels.cuh -- kernel parameter blocks and host launchers.
+#pragma once
+
+#include <cstdint>
+
+#include "fl_geometry.cuh"
+#include "fl_internal.cuh"
+
+namespace fl {
+
+struct ColParams {
+    int32_t n_nodes, n_elems;
+    int64_t n_tiles;
+    const double* nodes;
+    const int32_t* elems;
+    const int8_t* flags;
+    const int32_t* inc_ptr;
+    const uint32_t* inc;
+    FieldDesc f, coef, g_dir, g_neu;
+    bool want_a, want_b, want_sys, need_lift, has_neumann;
+    const int8_t* is_dir;
+    const int8_t* is_neu;
+    const int32_t* fidx;
+    int32_t* col_ptr;
+    int32_t* row_idx;
+    double* values;
+    double* b;
+    double* u0;
+    double* b_mod;
+    int32_t* ff_col_ptr;
+    int32_t* ff_row_idx;
+    double* ff_values;
+    double* b_f;
+    uint64_t* tile_status;
+    unsigned int* ticket;
+    uint32_t* err;
+    int64_t cap_a, cap_ff;
+};
+
+int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);
+int launch_validate(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);
+int launch_partition(fl_ctx* ctx, fl_mesh* mesh, fl_result* res);
+int launch_columns(fl_ctx* ctx, int dim, ColParams& p);
+int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
+                     const int32_t* row_idx, const double* values, int32_t n_rows,
+                     const int32_t* rows, int32_t n_cols, const int32_t* cols, fl_result* res,
+                     int32_t* row_map, int32_t* cnt, uint32_t* d_err, int64_t* nnz_out);
+int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
+                        double* qi);
+size_t column_smem_bytes();
+int column_tile_width();
+
+}  // namespace fl
