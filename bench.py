@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: P1 stiffness+load assembly (+ Dirichlet system) on B200.
+
+One "step" = one pass of the hot path over the configuration's mesh, exactly
+what solve_poisson builds before its solve (solver.hpp:226-242):
+partition_boundary + assemble_blockwise + assemble_load + apply_neumann +
+apply_dirichlet + submatrix(A, free, free) + b_f, INCLUDING the topology plan
+(node -> element incidence lists) rebuilt from the raw arrays every step
+(FL_REPLAN: a cold mesh, nothing cached across steps except device buffers).
+
+  value      elements/s with inputs resident in HBM (CUDA events per step, max
+             over ranks);
+  e2e        the same through the C-ABI with HOST buffers: H2D of the mesh arrays
+             from pinned memory, assembly, D2H of every output array;
+  roofline   the dominant kernel (k_columns) against the measured HBM copy peak;
+  cpu_baseline / --impl reference
+             the reference's own CPU path (oracle/_ref = femlite compiled from
+             its headers) on a bounded sample of the same workload family.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
+       python bench.py --impl reference ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DEFAULT_CONFIG = "C5"
+METRIC = "P1 stiffness+load assembly elements/sec and achieved HBM GB/s vs peak, 1/2/4/8 GPU"
+UNIT = "elements/s"
+L2_BYTES = 126 * 2 ** 20
+
+# bounded CPU samples (same family, smaller n): ~10-30 s of reference work
+CPU_SAMPLE_N = {"C1": 128, "C2": 512, "C3": 1024, "C4": 64, "C5": 64}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            if self._stop.is_set():
+                break
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        self._stop.set()
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if s[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = None):
+    """Time femlite's own solve_poisson pre-solve path (oracle/_ref) on a sample."""
+    from oracle import pyoracle as po
+    from paper_1804_05156_b200 import configs
+    if not po.have_ref():
+        return None
+    n = CPU_SAMPLE_N[config]
+    cfg = configs.build(config, n=n)
+    m = cfg.mesh
+    coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
+    f_kind = po.FIELD_SINSIN if cfg.f == "sinsin" else po.FIELD_CONST
+    f_val = 0.0 if cfg.f == "sinsin" else float(cfg.f)
+    secs, nnz, nnz_ff = po.ref_time_system(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val,
+                                           coef, reps=1)
+    one = float(secs[0])
+    if reps is None:
+        reps = max(1, min(5, int(seconds_budget / max(one, 1e-6))))
+    if reps > 1:
+        secs, nnz, nnz_ff = po.ref_time_system(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val,
+                                               coef, reps=reps)
+    med = float(np.median(secs))
+    return {"value": m.num_elems() / med, "unit": UNIT, "cores": 1, "kind": "reference",
+            "seconds_per_step": med, "reps": int(len(secs)), "n_elems": m.num_elems(),
+            "sample": (f"{cfg.description} (n={n}, NT={m.num_elems()}, nnz={nnz}): femlite "
+                       "partition_boundary+assemble_blockwise+assemble_load+apply_neumann+"
+                       "apply_dirichlet+submatrix+b_f, 1 thread (the reference is single-threaded)")}
+
+
+def run_reference_impl(args, rank: int, world: int):
+    if rank != 0:
+        return
+    from oracle import pyoracle as po
+    if not po.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    per_step = []
+    base = None
+    for s in range(args.warmup + args.steps):
+        r = cpu_reference(args.config, reps=1)
+        if s >= args.warmup:
+            per_step.append(r["seconds_per_step"])
+            base = r
+    ms = 1e3 * float(np.mean(per_step))
+    value = base["n_elems"] / (ms * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config} sample", "sample": base["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": base["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# GPU path
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.setdefault("FL_PROFILE", "1")
+    import paper_1804_05156_b200 as fl
+    from paper_1804_05156_b200 import _lib, configs
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    L = _lib.lib()
+    ctx = fl.Context(dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    t0 = time.time()
+    cfg = configs.build(args.config, f_mode="samples")
+    m = cfg.mesh
+    N, NT, d = m.num_nodes(), m.num_elems(), m.dim
+    log(f"[bench] {args.config}: {cfg.description} N={N} NT={NT} built in {time.time() - t0:.1f}s")
+
+    # device-resident inputs (uploaded once, untimed)
+    dm = m.device(ctx)
+    res = fl.AssemblyResult(ctx)
+    what = _lib.OUT_SYSTEM | _lib.REPLAN
+
+    def fields():
+        ff, k1 = fl.api._field_struct(cfg.f, m, "load")
+        fc, k2 = fl.api._field_struct(cfg.coef, m, "coef")
+        fd, k3 = fl.api._field_struct(cfg.g_dirichlet, m, "dirichlet")
+        fn, k4 = fl.api._field_struct(cfg.g_neumann, m, "neumann")
+        return (ff, fc, fd, fn), (k1, k2, k3, k4)
+
+    # f samples: stage once on the device so the timed steps read them from HBM
+    (ff, fc, fd, fn), keep = fields()
+    f_dev = None
+    if ff.kind == _lib.FIELD_SAMPLES:
+        f_dev = torch.from_numpy(np.asarray(keep[0])).to(f"cuda:{dev}")
+        ff.mem, ff.samples = _lib.MEM_DEVICE, f_dev.data_ptr()
+
+    def step():
+        _lib.check(L.fl_assemble(ctx.handle, dm.handle, C.byref(ff), C.byref(fc), C.byref(fd),
+                                 C.byref(fn), what, res.handle), "fl_assemble")
+
+    flush = None
+    ws_bytes = configs.system_bytes(d, N, NT, 0, 0, 0)
+    if ws_bytes < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+            sz = res.sizes()
+        ctx.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = ctx.launch_count()
+        clocks = ClockSampler(dev)
+        clocks.start()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        phase = []
+        for k in range(args.steps):
+            if flush is not None:
+                flush.fill_(k)
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            sz = res.sizes()  # synchronises; resolves the phase events
+            phase.append(ctx.last_timings())
+        torch.cuda.synchronize()
+        clocks.stop()
+        launches = ctx.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    col_ms = float(np.mean([p[2] for p in phase]))
+    plan_ms = float(np.mean([p[0] for p in phase]))
+    mark_ms = float(np.mean([p[1] for p in phase]))
+
+    nnz, nnz_ff, n_free = int(sz.nnz), int(sz.nnz_ff), int(sz.n_free)
+    b_sl = configs.algorithmic_bytes(d, N, NT, nnz)
+    b_sys = configs.system_bytes(d, N, NT, nnz, n_free, nnz_ff)
+    f_bytes = 8 * NT * (d + 1) if ff.kind == _lib.FIELD_SAMPLES else 0
+    # k_columns algorithmic bytes: mesh + plan-free inputs + every output it writes
+    col_bytes = (4 * (d + 1) * NT + 8 * d * N + f_bytes + N + 4 * N  # elems, nodes, f, is_dir, fidx
+                 + 4 * (N + 1) + 12 * nnz + 8 * N + 16 * N             # A, b, u0, b_mod
+                 + 4 * (n_free + 1) + 12 * nnz_ff + 8 * n_free)        # A_ff, b_f
+    peak, peak_kind = peaks()
+    achieved = col_bytes / (col_ms * 1e-3) / 1e9
+
+    # ---- e2e through the C-ABI with host buffers (pinned) ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev)
+
+    line = None
+    if rank == 0:
+        # replicas: every rank assembles the whole mesh (sharded path: see DESIGN.md §6)
+        value = world * NT / (ms * 1e-3)
+        cpu = None if args.no_cpu_baseline else cpu_reference(args.config)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator meshes, SURVEY.md §8(d) recipes)",
+            "config": {"workload": f"{args.config}: {cfg.description}", "n_nodes": N,
+                       "n_elems": NT, "nnz": nnz, "nnz_ff": nnz_ff, "n_free": n_free,
+                       "step": "plan+partition+stiffness+load+dirichlet+A_ff+b_f",
+                       "l2": ("flushed between steps (256 MB write)" if flush is not None
+                              else "inputs larger than L2"),
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "f": str(cfg.f) if not isinstance(cfg.f, np.ndarray) else "host samples",
+                       "coef": str(cfg.coef)},
+            "hbm_gbs_step": b_sys / (ms * 1e-3) / 1e9,
+            "bytes": {"B_SL": b_sl, "B_sys": b_sys, "f_samples": f_bytes, "k_columns": col_bytes},
+            "phases_ms": {"plan": plan_ms, "partition": mark_ms, "k_columns": col_ms},
+            "roofline": {"bound": "hbm", "kernel": "k_columns", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        if args.traffic:
+            line["roofline"]["traffic"] = float(args.traffic)
+        print(json.dumps(line))
+    return line
+
+
+def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev):
+    m = cfg.mesh
+    N, NT, d = m.num_nodes(), m.num_elems(), m.dim
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.int32: torch.int32,
+                                        np.int8: torch.int8}[a.dtype.type], pin_memory=True)
+        t.numpy()[...] = a
+        return t
+
+    h_nodes, h_elems, h_flags = pinned(m.nodes), pinned(m.elems), pinned(m.bd_flags)
+    f_arr = np.asarray(cfg.f) if isinstance(cfg.f, np.ndarray) else None
+    h_f = pinned(f_arr) if f_arr is not None else None
+    # a separate fl_mesh fed from host memory every step
+    hmesh = C.c_void_p()
+    _lib.check(L.fl_mesh_create(ctx.handle, d, N, NT, h_nodes.data_ptr(), h_elems.data_ptr(),
+                                h_flags.data_ptr(), _lib.MEM_HOST, C.byref(hmesh)))
+    res = fl.AssemblyResult(ctx)
+    ff, _k1 = fl.api._field_struct(cfg.f if f_arr is None else None, m, "load")
+    if f_arr is not None:
+        ff.kind, ff.mem, ff.samples, ff.n_samples = _lib.FIELD_SAMPLES, _lib.MEM_HOST, h_f.data_ptr(), f_arr.size
+    fc, _k2 = fl.api._field_struct(cfg.coef, m, "coef")
+    fd, _k3 = fl.api._field_struct(cfg.g_dirichlet, m, "dirichlet")
+    fn, _k4 = fl.api._field_struct(cfg.g_neumann, m, "neumann")
+    outs = None
+
+    def e2e_step():
+        nonlocal outs
+        _lib.check(L.fl_mesh_set_nodes(ctx.handle, hmesh, h_nodes.data_ptr(), _lib.MEM_HOST))
+        _lib.check(L.fl_mesh_set_elems(ctx.handle, hmesh, h_elems.data_ptr(), _lib.MEM_HOST))
+        _lib.check(L.fl_mesh_set_flags(ctx.handle, hmesh, h_flags.data_ptr(), _lib.MEM_HOST))
+        _lib.check(L.fl_assemble(ctx.handle, hmesh, C.byref(ff), C.byref(fc), C.byref(fd),
+                                 C.byref(fn), _lib.OUT_SYSTEM, res.handle))
+        sz = res.sizes()
+        if outs is None:
+            spec = [(_lib.A_COL_PTR, torch.int32, N + 1), (_lib.A_ROW_IDX, torch.int32, sz.nnz),
+                    (_lib.A_VALUES, torch.float64, sz.nnz), (_lib.B, torch.float64, N),
+                    (_lib.U0, torch.float64, N), (_lib.B_MOD, torch.float64, N),
+                    (_lib.DIR_NODES, torch.int32, sz.n_dir), (_lib.FREE_NODES, torch.int32, sz.n_free),
+                    (_lib.AFF_COL_PTR, torch.int32, sz.n_free + 1),
+                    (_lib.AFF_ROW_IDX, torch.int32, sz.nnz_ff),
+                    (_lib.AFF_VALUES, torch.float64, sz.nnz_ff), (_lib.B_F, torch.float64, sz.n_free)]
+            outs = [(w, torch.empty(max(c, 1), dtype=t, pin_memory=True)) for w, t, c in spec]
+        for w, buf in outs:
+            _lib.check(L.fl_result_copy(res.handle, w, buf.data_ptr(),
+                                        buf.numel() * buf.element_size(), _lib.MEM_HOST))
+        return sz
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup)):
+            sz = e2e_step()
+        times = []
+        for _ in range(max(1, min(args.steps, args.e2e_steps))):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            sz = e2e_step()
+            ctx.synchronize()
+            times.append(time.perf_counter() - t0)
+    L.fl_mesh_destroy(hmesh)
+    h2d = h_nodes.numel() * 8 + h_elems.numel() * 4 + h_flags.numel() + (f_arr.nbytes if f_arr is not None else 0)
+    d2h = sum(buf.numel() * buf.element_size() for _, buf in outs)
+    sec = float(np.mean(times))
+    return {"value": NT / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3,
+            "timing": "wall clock per step, synchronised, host arrays in pinned memory"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per k_columns launch (from profiles/), echoed into roofline")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.warmup < 3:
+        log("[bench] warning: fewer than 3 warm-up steps")
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference_impl(args, rank, world)
+        return
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

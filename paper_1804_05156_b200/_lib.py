@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libfemlite_b200.so")
 # enum fl_mem / fl_field_kind / fl_output / fl_array (femlite_b200.h)
 MEM_HOST, MEM_DEVICE = 0, 1
 FIELD_NONE, FIELD_CONST, FIELD_SINSIN, FIELD_X, FIELD_XYZ, FIELD_SAMPLES, FIELD_COEF_C5 = 0, 1, 2, 3, 4, 6, 7
-OUT_STIFFNESS, OUT_LOAD, OUT_PARTITION, OUT_SYSTEM = 1, 2, 4, 8
+OUT_STIFFNESS, OUT_LOAD, OUT_PARTITION, OUT_SYSTEM, REPLAN = 1, 2, 4, 8, 16
 (A_COL_PTR, A_ROW_IDX, A_VALUES, B, U0, B_MOD, DIR_NODES, FREE_NODES,
  AFF_COL_PTR, AFF_ROW_IDX, AFF_VALUES, B_F) = range(12)
 
@@ -36,6 +36,7 @@ SIGNATURES = {
                                  C.POINTER(_vp)]),
     "fl_mesh_set_nodes": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "fl_mesh_set_flags": (C.c_int, [_vp, _vp, _vp, C.c_int]),
+    "fl_mesh_set_elems": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "fl_mesh_validate": (C.c_int, [_vp, _vp]),
     "fl_mesh_plan": (C.c_int, [_vp, _vp]),
     "fl_mesh_destroy": (C.c_int, [_vp]),

@@ -232,6 +232,13 @@ FL_API int fl_mesh_set_flags(fl_ctx* ctx, fl_mesh* mesh, const int8_t* bd_flags,
     return copy_in(ctx, mesh->flags, bd_flags, (size_t)mesh->n_elems * (mesh->dim + 1), mem);
 }
 
+FL_API int fl_mesh_set_elems(fl_ctx* ctx, fl_mesh* mesh, const int32_t* elems, int mem) {
+    if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    mesh->planned = false;
+    return copy_in(ctx, mesh->elems, elems, sizeof(int32_t) * (size_t)mesh->n_elems * (mesh->dim + 1),
+                   mem);
+}
+
 FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     if (!mesh) return FL_OK;
     if (mesh->ctx) cudaStreamSynchronize(mesh->ctx->stream);
@@ -330,6 +337,8 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     if (!ctx || !mesh || !res) return set_error(FL_ERR_ARGUMENT, "null argument");
     if (!field_ok(f) || !field_ok(coef) || !field_ok(g_dirichlet) || !field_ok(g_neumann))
         return set_error(FL_ERR_ARGUMENT, "invalid field descriptor");
+    const bool replan = what & FL_REPLAN;
+    what &= ~(uint32_t)FL_REPLAN;
     if (what & FL_OUT_SYSTEM) what |= FL_OUT_STIFFNESS | FL_OUT_LOAD | FL_OUT_PARTITION;
     if (what == 0) return set_error(FL_ERR_ARGUMENT, "nothing requested");
     FL_CUDA(cudaSetDevice(ctx->device));
@@ -338,6 +347,11 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     ctx->plan_timed = false;
     if (!mesh->planned && (what & (FL_OUT_STIFFNESS | FL_OUT_LOAD))) {
         FL_TRY(fl_mesh_plan(ctx, mesh));
+        ctx->plan_timed = true;
+    } else if (replan && (what & (FL_OUT_STIFFNESS | FL_OUT_LOAD))) {
+        // same topology: rebuild asynchronously (the output bound is unchanged)
+        uint32_t* d_err = reinterpret_cast<uint32_t*>(mesh->stats.as<unsigned long long>() + 3);
+        FL_TRY(launch_plan_kernels(ctx, mesh, d_err));
         ctx->plan_timed = true;
     }
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
