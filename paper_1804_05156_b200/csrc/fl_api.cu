@@ -106,7 +106,29 @@ struct fl_result_ext {
     ResultStage stage;
     bool g_missing = false;
     bool partition_done = false;
+    // last column launch, kept for the general-kernel fallback
+    ColParams last{};
+    fl_mesh* last_mesh = nullptr;
+    bool last_valid = false;
 };
+
+// Re-run the column pass on the general warp-per-column kernel (a tile or a
+// column exceeded the tiled kernel's shared-memory limits).
+static int rerun_general(fl_result* res, fl_result_ext* x) {
+    fl_ctx* ctx = res->ctx;
+    fl_mesh* mesh = x->last_mesh;
+    ColParams p = x->last;
+    uint32_t* counters = res->counters.as<uint32_t>();
+    FL_TRY(launch_inc_sort(ctx, mesh));
+    FL_CUDA(cudaMemsetAsync(counters + CNT_TICKET, 0, sizeof(uint32_t), ctx->stream));
+    FL_CUDA(cudaMemsetAsync(counters + CNT_ERR, 0, sizeof(uint32_t), ctx->stream));
+    const int tw = column_tile_width();
+    p.n_tiles = (mesh->n_nodes + tw - 1) / tw;
+    FL_CUDA(cudaMemsetAsync(res->tile_status.p, 0, sizeof(uint64_t) * ((size_t)p.n_tiles + 1),
+                            ctx->stream));
+    FL_TRY(launch_columns(ctx, mesh->dim, p));
+    return FL_OK;
+}
 static fl_result_ext* ext_of(fl_result* r) {
     return reinterpret_cast<fl_result_ext*>(reinterpret_cast<char*>(r) + sizeof(fl_result));
 }
@@ -451,7 +473,18 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         p.err = counters + CNT_ERR;
         p.cap_a = want_a ? (int64_t)cap : 0;
         p.cap_ff = want_sys ? (int64_t)cap : 0;
-        if (N > 0) FL_TRY(launch_columns(ctx, mesh->dim, p));
+        x->last = p;
+        x->last_mesh = mesh;
+        x->last_valid = true;
+        if (N > 0) {
+            const char* kern = std::getenv("FL_KERNEL");
+            if (kern && kern[0] == '1') {
+                FL_TRY(launch_inc_sort(ctx, mesh));
+                FL_TRY(launch_columns(ctx, mesh->dim, p));
+            } else {
+                FL_TRY(launch_columns2(ctx, mesh->dim, p));
+            }
+        }
     }
     if (ctx->profile) {
         FL_CUDA(cudaEventRecord(ctx->ev[3], s));
@@ -475,6 +508,15 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
             FL_CUDA(cudaMemcpyAsync(&hn[0], res->arr[FL_A_COL_PTR].as<int32_t>() + res->n,
                                     sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         FL_CUDA(cudaStreamSynchronize(s));
+        if ((h[CNT_ERR] & DERR_V2_OVERFLOW) && x->last_valid) {
+            FL_TRY(rerun_general(res, x));
+            FL_CUDA(cudaMemcpyAsync(h, res->counters.p, sizeof(uint32_t) * CNT_WORDS,
+                                    cudaMemcpyDeviceToHost, s));
+            if ((res->what & FL_OUT_STIFFNESS) && res->arr[FL_A_COL_PTR].p)
+                FL_CUDA(cudaMemcpyAsync(&hn[0], res->arr[FL_A_COL_PTR].as<int32_t>() + res->n,
+                                        sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            FL_CUDA(cudaStreamSynchronize(s));
+        }
         fl_sizes z{};
         z.n = res->n;
         z.nnz = hn[0];

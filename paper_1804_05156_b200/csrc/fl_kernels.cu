@@ -763,11 +763,22 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         count_launch(ctx);
     }
     if (N > 0) {
-        k_inc_sort<<<div_up(N, 128), 128, 0, s>>>(N, mesh->inc_ptr.as<int32_t>(),
-                                                  mesh->inc.as<uint32_t>());
         k_plan_stats<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(
             N, mesh->dim, mesh->inc_ptr.as<int32_t>(), mesh->stats.as<unsigned long long>());
-        count_launch(ctx, 2);
+        count_launch(ctx);
+    }
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// The general kernel needs each node's incidences in (j, t) order; the tiled
+// kernel ranks them itself, so this pass only runs on the fallback path.
+int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh) {
+    const int32_t N = mesh->n_nodes;
+    if (N > 0) {
+        k_inc_sort<<<div_up(N, 128), 128, 0, ctx->stream>>>(N, mesh->inc_ptr.as<int32_t>(),
+                                                           mesh->inc.as<uint32_t>());
+        count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
     return FL_OK;
