@@ -1,21 +1,26 @@
 // fl_columns2.cu -- the tiled column kernel (v2), the fast path of fl_assemble.
 //
 // One CTA assembles a tile of TC consecutive output columns (= reference CSC
-// columns) in four phases:
-//   1. incidence keys of the tile -> smem (unsorted, straight from the plan);
-//   2. lane-per-incidence: rank of the key inside its column (the (j, t) order of
-//      assembly.hpp:486-498 after sparse.hpp:79-89's stable passes), element
-//      geometry for column j (fl_geometry.cuh), s_ij (i = 0..d) and the load
-//      share, written to smem at the ranked position;
-//   3. thread-per-column: b = 0 + sum of load shares in (j, t) order
-//      (system.hpp:114-118); every entry (r, c) folded sequentially in the
-//      reference order (i, j, t) (sweep i outer, ranked incidences inner);
-//      optional transposed folds for the Dirichlet lift; zero drop
-//      (sparse.hpp:105); A(free, free) rows; b, u0, b_mod, b_f;
-//   4. CTA offsets by decoupled look-back, coalesced copy of the tile's entries.
-// Columns that do not fit (too many incidences per tile / distinct rows per
-// column) raise DERR_V2_OVERFLOW and the host reruns the mesh on the general
-// warp-per-column kernel (fl_kernels.cu k_columns).
+// columns; the pattern is symmetric, so also CSR rows) in four phases:
+//   1. the tile's incidence keys (j << 30 | t) -> smem, unsorted from the plan;
+//   2. lane per incidence: rank of the key inside its column = the (j, t) order in
+//      which the reference's blockwise triplets reach that column
+//      (assembly.hpp:486-498 + the stable passes sparse.hpp:79-89); element
+//      geometry for column j (fl_geometry.cuh) -> s_ij (i = 0..d) and the load
+//      share, stored at [rank][i][column] (column-interleaved: conflict-free);
+//   3. P threads per column; thread u owns the distinct rows whose hash selects u
+//      and sweeps the column's items in the reference order (i outer, ranked
+//      incidence inner) folding only its own rows, so every entry (r, c) is the
+//      sequential sum of sparse.hpp:98-104 in (i*(d+1)+j, t) order.  Thread 0 of
+//      the column also folds b (0.0 + shares in (j, t) order, system.hpp:114-118)
+//      and the Neumann data; optional transposed folds give A(c, r) for the
+//      Dirichlet lift (matvec sparse.hpp:129-141);
+//   4. merge the P slot lists, sort rows, drop exact zeros (sparse.hpp:105),
+//      A(free, free) rows, CTA offsets by a warp-wide decoupled look-back,
+//      coalesced copy of the tile's entries; b, u0, b_mod, b_f per column.
+// A column with more than KMAX incidences or more distinct rows than the slot
+// tables hold raises DERR_V2_OVERFLOW; the host then reruns the mesh on the
+// general warp-per-column kernel (fl_kernels.cu k_columns).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -28,86 +33,60 @@
 
 namespace fl {
 
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
 template <int D>
 struct Tile;
 template <>
 struct Tile<2> {
-    static constexpr int TC = 64;      // columns per tile
-    static constexpr int CAP = 768;    // incidences per tile
-    static constexpr int HS = 16;      // slot table per column (distinct rows)
-    static constexpr int MAXS = 12;    // max distinct rows accepted (load 0.75)
+    static constexpr int TC = 64;       // columns per tile
     static constexpr int THREADS = 128;
+    static constexpr int HSU = 8;       // slot table entries per (column, owner thread)
+    static constexpr int MAXU = 6;      // distinct rows per owner thread (load 0.75)
+    static constexpr int MAXS = 12;     // distinct rows per column
 };
 template <>
 struct Tile<3> {
     static constexpr int TC = 32;
-    static constexpr int CAP = 1024;
-    static constexpr int HS = 32;
-    static constexpr int MAXS = 24;
     static constexpr int THREADS = 128;
+    static constexpr int HSU = 8;
+    static constexpr int MAXU = 6;
+    static constexpr int MAXS = 24;
 };
 
-template <int D>
-struct TileSmem {
+template <int D, int KMAX, bool LIFT>
+struct Layout {
     using T = Tile<D>;
     static constexpr int NV = D + 1;
-    // phase 1/2 buffers (reused for the output lists after the fold)
-    union {
-        struct {
-            double S[T::CAP][NV];  // s_ij for i = 0..D, ranked incidence order
-            double Lb[T::CAP];     // load share
-            int32_t R[T::CAP][NV]; // element vertices (rows)
-            uint32_t ks[T::CAP];   // ranked keys (j << 30 | t)
-        } in;
-        struct {
-            int32_t a_row[T::MAXS][T::TC];
-            double a_val[T::MAXS][T::TC];
-            int32_t f_row[T::MAXS][T::TC];
-            double f_val[T::MAXS][T::TC];
-        } out;
-    } u;
-    uint32_t key[T::CAP];          // unsorted keys
-    int32_t ptr[T::TC + 1];
-    int32_t tab_row[T::HS][T::TC];
-    double tab_acc[T::HS][T::TC];
-    double tab_tacc[T::HS][T::TC];
-    int32_t na[T::TC + 1], nf[T::TC + 1];
-    int64_t off_a, off_f;
-    int32_t total_a, total_f;
-    int32_t bad;
+    static constexpr int TC = T::TC;
+    static constexpr int P = T::THREADS / T::TC;  // threads per column
+    static constexpr int SROW = NV * TC + 1;      // padded stride of one rank row
+    static constexpr int LROW = TC + 1;
+    // byte offsets of the dynamic smem carve-up
+    static constexpr size_t S_OFF = 0;                                          // double [KMAX][SROW]
+    static constexpr size_t R_OFF = S_OFF + sizeof(double) * KMAX * SROW;       // int32 [KMAX][SROW]
+    static constexpr size_t L_OFF = (R_OFF + sizeof(int32_t) * KMAX * SROW + 7) & ~size_t(7);
+    static constexpr size_t KS_OFF = L_OFF + sizeof(double) * KMAX * LROW;      // uint32 [KMAX][LROW]
+    static constexpr size_t IN_END = KS_OFF + sizeof(uint32_t) * KMAX * LROW;
+    // output lists alias the phase-2 buffers after the folds
+    static constexpr size_t M_ROW = 0;                                          // int32 [MAXS][TC]
+    static constexpr size_t M_VAL = M_ROW + sizeof(int32_t) * T::MAXS * TC;     // double
+    static constexpr size_t M_TV = M_VAL + sizeof(double) * T::MAXS * TC;       // double
+    static constexpr size_t F_ROW = M_TV + sizeof(double) * T::MAXS * TC;       // int32
+    static constexpr size_t F_VAL = F_ROW + sizeof(int32_t) * T::MAXS * TC;     // double
+    static constexpr size_t OUT_END = F_VAL + sizeof(double) * T::MAXS * TC;
+    static constexpr size_t UNION_END = IN_END > OUT_END ? IN_END : OUT_END;
+    static constexpr size_t KEY_OFF = (UNION_END + 15) & ~size_t(15);           // uint32 [TC*KMAX]
+    static constexpr size_t TR_OFF = KEY_OFF + sizeof(uint32_t) * TC * KMAX;    // int32 [HSU][THREADS]
+    static constexpr size_t TA_OFF = TR_OFF + sizeof(int32_t) * T::HSU * T::THREADS;  // double
+    static constexpr size_t TT_OFF = TA_OFF + sizeof(double) * T::HSU * T::THREADS;   // double (LIFT)
+    static constexpr size_t TAB_END = TT_OFF + (LIFT ? sizeof(double) * T::HSU * T::THREADS : 0);
+    static constexpr size_t PTR_OFF = TAB_END;                                   // int32 [TC+1]
+    static constexpr size_t NA_OFF = PTR_OFF + sizeof(int32_t) * (TC + 1);      // int32 [TC+1]
+    static constexpr size_t NF_OFF = NA_OFF + sizeof(int32_t) * (TC + 1);       // int32 [TC+1]
+    static constexpr size_t MISC_OFF = (NF_OFF + sizeof(int32_t) * (TC + 1) + 15) & ~size_t(15);
+    static constexpr size_t BYTES = MISC_OFF + 64;
 };
-
-template <int D>
-size_t tile_smem_bytes() { return sizeof(TileSmem<D>); }
-
-__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
-
-template <int D>
-__device__ __forceinline__ int tab_find_or_insert(TileSmem<D>& sm, int col, int32_t row, int& n) {
-    constexpr int HS = Tile<D>::HS;
-    uint32_t h = ((uint32_t)row * 2654435761u) >> (32 - ilog2(HS));
-    while (true) {
-        const int32_t k = sm.tab_row[h][col];
-        if (k == row) return (int)h;
-        if (k == -1) {
-            if (n >= Tile<D>::MAXS) return -1;  // table at its load limit: overflow
-            sm.tab_row[h][col] = row;
-            sm.tab_acc[h][col] = -0.0;  // -0.0 + x == x: the fold starts at its first value
-            sm.tab_tacc[h][col] = -0.0;
-            ++n;
-            return (int)h;
-        }
-        h = (h + 1) & (HS - 1);
-    }
-}
-
-template <int D>
-__device__ __forceinline__ int tab_find(const TileSmem<D>& sm, int col, int32_t row) {
-    constexpr int HS = Tile<D>::HS;
-    uint32_t h = ((uint32_t)row * 2654435761u) >> (32 - ilog2(HS));
-    while (sm.tab_row[h][col] != row) h = (h + 1) & (HS - 1);
-    return (int)h;
-}
 
 __device__ __forceinline__ double node_field(const FieldDesc& g, const double* nodes, int dim,
                                              int32_t k) {
@@ -119,59 +98,81 @@ __device__ __forceinline__ double node_field(const FieldDesc& g, const double* n
     return eval_point(g, x, y, z);
 }
 
-template <int D>
+template <int D, int KMAX, bool LIFT>
 __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
     using T = Tile<D>;
+    using LY = Layout<D, KMAX, LIFT>;
     constexpr int NV = D + 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem<D>& sm = *reinterpret_cast<TileSmem<D>*>(smem_raw);
-    __shared__ int64_t s_tile;
+    constexpr int TC = T::TC;
+    constexpr int P = LY::P;
+    constexpr int LOGP = ilog2(P);
+    constexpr int LOGH = ilog2(T::HSU);
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* S = reinterpret_cast<double*>(smem + LY::S_OFF);
+    int32_t* R = reinterpret_cast<int32_t*>(smem + LY::R_OFF);
+    double* Lb = reinterpret_cast<double*>(smem + LY::L_OFF);
+    uint32_t* KS = reinterpret_cast<uint32_t*>(smem + LY::KS_OFF);
+    int32_t* o_row = reinterpret_cast<int32_t*>(smem + LY::M_ROW);
+    double* o_val = reinterpret_cast<double*>(smem + LY::M_VAL);
+    double* o_tv = reinterpret_cast<double*>(smem + LY::M_TV);
+    int32_t* f_row = reinterpret_cast<int32_t*>(smem + LY::F_ROW);
+    double* f_val = reinterpret_cast<double*>(smem + LY::F_VAL);
+    uint32_t* key = reinterpret_cast<uint32_t*>(smem + LY::KEY_OFF);
+    int32_t* tab_row = reinterpret_cast<int32_t*>(smem + LY::TR_OFF);
+    double* tab_acc = reinterpret_cast<double*>(smem + LY::TA_OFF);
+    double* tab_tacc = reinterpret_cast<double*>(smem + LY::TT_OFF);
+    int32_t* ptr = reinterpret_cast<int32_t*>(smem + LY::PTR_OFF);
+    int32_t* na = reinterpret_cast<int32_t*>(smem + LY::NA_OFF);
+    int32_t* nf = reinterpret_cast<int32_t*>(smem + LY::NF_OFF);
+    int64_t* misc = reinterpret_cast<int64_t*>(smem + LY::MISC_OFF);  // tile, off_a, off_f, bad
+
     const int tid = threadIdx.x;
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
+    // phase-3 identity: column `col`, owner slot `u`
+    const int col = tid >> LOGP;
+    const int u = tid & (P - 1);
 
     while (true) {
-        if (tid == 0) s_tile = atomicAdd(p.ticket, 1u);
+        if (tid == 0) misc[0] = atomicAdd(p.ticket, 1u);
         __syncthreads();
-        const int64_t tile = s_tile;
+        const int64_t tile = misc[0];
         if (tile >= p.n_tiles) break;
-        const int32_t c0 = (int32_t)(tile * T::TC);
-        const int ncols = min(T::TC, p.n_nodes - c0);
+        const int32_t c0 = (int32_t)(tile * TC);
+        const int ncols = min(TC, p.n_nodes - c0);
 
-        // ---- phase 1: keys of the tile
+        // ---- phase 1: the tile's incidence keys
         const int32_t base = __ldg(p.inc_ptr + c0);
-        if (tid <= T::TC) {
-            const int cc = min(tid, ncols);
-            sm.ptr[tid] = __ldg(p.inc_ptr + c0 + cc) - base;
-        }
-        if (tid == 0) sm.bad = 0;
+        if (tid <= TC) ptr[tid] = __ldg(p.inc_ptr + c0 + min(tid, ncols)) - base;
+        if (tid == 0) misc[3] = 0;
         __syncthreads();
-        const int M = sm.ptr[ncols];
-        if (M > T::CAP) {
+        const int M = ptr[ncols];
+        bool too_big = false;
+        if (tid < ncols) too_big = ptr[tid + 1] - ptr[tid] > KMAX;
+        if (__syncthreads_or(too_big)) {
             if (tid == 0) atomicOr(p.err, DERR_V2_OVERFLOW);
-            // keep the look-back chain alive
-            if (tid == 0) lookback(p.tile_status, tile, 0);
+            if (tid < 32) warp_lookback(p.tile_status, tile, 0);  // keep the chain alive
             __syncthreads();
             continue;
         }
-        for (int q = tid; q < M; q += T::THREADS) sm.key[q] = __ldg(p.inc + base + q);
+        for (int q = tid; q < M; q += T::THREADS) key[q] = __ldg(p.inc + base + q);
         __syncthreads();
 
         // ---- phase 2: rank + geometry, lane per incidence
         for (int q = tid; q < M; q += T::THREADS) {
-            const uint32_t key = sm.key[q];
-            int lo = 0, hi = ncols;  // column: ptr[col] <= q < ptr[col+1]
+            const uint32_t kq = key[q];
+            int lo = 0, hi = ncols;  // column of q: ptr[lo] <= q < ptr[lo + 1]
+#pragma unroll 1
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
-                if (sm.ptr[mid] <= q) lo = mid;
+                if (ptr[mid] <= q) lo = mid;
                 else hi = mid;
             }
-            const int pb = sm.ptr[lo], pe = sm.ptr[lo + 1];
+            const int pb = ptr[lo], pe = ptr[lo + 1];
             int rank = 0;
-            for (int r = pb; r < pe; ++r) rank += sm.key[r] < key;
-            const int pos = pb + rank;
-            const int32_t t = (int32_t)(key & 0x3FFFFFFFu);
-            const int j = (int)(key >> 30);
+            for (int r = pb; r < pe; ++r) rank += key[r] < kq;
+            const int32_t t = (int32_t)(kq & 0x3FFFFFFFu);
+            const int j = (int)(kq >> 30);
             int32_t V[NV];
             if constexpr (D == 3) {
                 const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
@@ -205,69 +206,95 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
             }
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
-                sm.u.in.S[pos][i] = s[i];
-                sm.u.in.R[pos][i] = V[i];
+                S[rank * LY::SROW + i * TC + lo] = s[i];
+                R[rank * LY::SROW + i * TC + lo] = V[i];
             }
-            sm.u.in.Lb[pos] = l;
-            sm.u.in.ks[pos] = key;
+            Lb[rank * LY::LROW + lo] = l;
+            KS[rank * LY::LROW + lo] = kq;
         }
         __syncthreads();
 
-        // ---- phase 3: thread per column, exact sequential folds
-        const int col = tid;
+        // ---- phase 3: folds, P threads per column
         const bool mine = col < ncols;
         const int32_t c = c0 + col;
+        const int m = mine ? ptr[col + 1] - ptr[col] : 0;
         double b = 0.0, y = 0.0;
-        int nslots = 0;
-        if (mine) {
-            const int pb = sm.ptr[col], pe = sm.ptr[col + 1];
-            if (p.want_b)
-                for (int k = pb; k < pe; ++k) b = b + sm.u.in.Lb[k];
-            if (p.want_a) {
+        int nown = 0;
+        if (mine && p.want_a) {
 #pragma unroll
-                for (int h = 0; h < T::HS; ++h) sm.tab_row[h][col] = -1;
-                for (int i = 0; i < NV; ++i)
-                    for (int k = pb; k < pe; ++k) {
-                        const int32_t r = sm.u.in.R[k][i];
-                        const int h = tab_find_or_insert<D>(sm, col, r, nslots);
-                        if (h < 0) {
-                            nslots = T::MAXS + 1;
+            for (int h = 0; h < T::HSU; ++h) tab_row[h * T::THREADS + tid] = -1;
+            bool over = false;
+            for (int i = 0; i < NV; ++i) {
+                for (int k = 0; k < m; ++k) {
+                    const int32_t r = R[k * LY::SROW + i * TC + col];
+                    const uint32_t hv = (uint32_t)r * 2654435761u;
+                    if (P > 1 && (int)(hv >> (32 - LOGP)) != u) continue;
+                    uint32_t h = (hv >> (32 - LOGP - LOGH)) & (T::HSU - 1);
+                    int slot = -1;
+                    while (true) {
+                        const int32_t kk = tab_row[h * T::THREADS + tid];
+                        if (kk == r) {
+                            slot = (int)h;
                             break;
                         }
-                        sm.tab_acc[h][col] = sm.tab_acc[h][col] + sm.u.in.S[k][i];
+                        if (kk == -1) {
+                            if (nown >= T::MAXU) break;
+                            tab_row[h * T::THREADS + tid] = r;
+                            tab_acc[h * T::THREADS + tid] = -0.0;  // -0.0 + x == x
+                            if (LIFT) tab_tacc[h * T::THREADS + tid] = -0.0;
+                            ++nown;
+                            slot = (int)h;
+                            break;
+                        }
+                        h = (h + 1) & (T::HSU - 1);
                     }
-                if (nslots > T::MAXS) sm.bad = 1;
-                if (p.need_lift && nslots <= T::MAXS) {
-                    // entry (c, r) in its own order (i_c*(d+1)+j_r, t): sweep j (= local
-                    // index of c, the ranked order's major key), then i, then t
-                    int k0 = pb;
-                    while (k0 < pe) {
-                        const uint32_t jb = sm.u.in.ks[k0] >> 30;
-                        int k1 = k0;
-                        while (k1 < pe && (sm.u.in.ks[k1] >> 30) == jb) ++k1;
-                        for (int i = 0; i < NV; ++i)
-                            for (int k = k0; k < k1; ++k) {
-                                const int h = tab_find<D>(sm, col, sm.u.in.R[k][i]);
-                                sm.tab_tacc[h][col] = sm.tab_tacc[h][col] + sm.u.in.S[k][i];
-                            }
-                        k0 = k1;
+                    if (slot < 0) {
+                        over = true;
+                        continue;
                     }
+                    double& a = tab_acc[slot * T::THREADS + tid];
+                    a = a + S[k * LY::SROW + i * TC + col];
                 }
             }
+            if (over) misc[3] = 1;
+            if (LIFT && !over) {
+                // entry (c, r) in its own order (i_c*(d+1)+j_r, t): j-buckets of the
+                // ranked incidences (j = local index of c) outer, then i, then t
+                int k0 = 0;
+                while (k0 < m) {
+                    const uint32_t jb = KS[k0 * LY::LROW + col] >> 30;
+                    int k1 = k0;
+                    while (k1 < m && (KS[k1 * LY::LROW + col] >> 30) == jb) ++k1;
+                    for (int i = 0; i < NV; ++i)
+                        for (int k = k0; k < k1; ++k) {
+                            const int32_t r = R[k * LY::SROW + i * TC + col];
+                            const uint32_t hv = (uint32_t)r * 2654435761u;
+                            if (P > 1 && (int)(hv >> (32 - LOGP)) != u) continue;
+                            uint32_t h = (hv >> (32 - LOGP - LOGH)) & (T::HSU - 1);
+                            while (tab_row[h * T::THREADS + tid] != r) h = (h + 1) & (T::HSU - 1);
+                            double& a = tab_tacc[h * T::THREADS + tid];
+                            a = a + S[k * LY::SROW + i * TC + col];
+                        }
+                    k0 = k1;
+                }
+            }
+        }
+        if (mine && u == 0) {
+            if (p.want_b)
+                for (int k = 0; k < m; ++k) b = b + Lb[k * LY::LROW + col];
             // Neumann data (system.hpp:123-172) at nodes on flag-2 faces: face-major
             // (lf, t) order, accumulated from 0.0, then b += add
             if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE && p.is_neu[c]) {
                 double add = 0.0;
                 for (int lf = 0; lf < NV; ++lf) {
                     int32_t last = -1;
-                    while (true) {  // next element t > last with a flag-2 face lf containing c
+                    while (true) {
                         int32_t best = INT_MAX;
                         int kb = -1;
-                        for (int k = pb; k < pe; ++k) {
-                            const uint32_t key = sm.u.in.ks[k];
-                            const int32_t t = (int32_t)(key & 0x3FFFFFFFu);
-                            const int j = (int)(key >> 30);
-                            if (j == lf || t <= last || t >= best) continue;
+                        for (int k = 0; k < m; ++k) {
+                            const uint32_t kq = KS[k * LY::LROW + col];
+                            const int32_t t = (int32_t)(kq & 0x3FFFFFFFu);
+                            if ((int)(kq >> 30) == lf || t <= last || t >= best) continue;
                             if (p.flags[(size_t)t * NV + lf] != 2) continue;
                             best = t;
                             kb = k;
@@ -276,7 +303,7 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
                         last = best;
                         int32_t V[NV];
 #pragma unroll
-                        for (int i = 0; i < NV; ++i) V[i] = sm.u.in.R[kb][i];
+                        for (int i = 0; i < NV; ++i) V[i] = R[kb * LY::SROW + i * TC + col];
                         ElemCol<D> ec;
                         ec.load(p.nodes, V);
                         add = add + ec.face_share(lf, p.g_neu, R3, best);
@@ -285,131 +312,179 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
                 b = b + add;
             }
         }
-        __syncthreads();  // all folds done: the input buffers become the output lists
-        if (tid == 0) sm.total_a = sm.total_f = 0;
-        if (mine && p.want_a) {
-            // extract slots, insertion-sort by row into the output lists
-            int n = 0;
-            if (nslots <= T::MAXS) {
-                for (int h = 0; h < T::HS; ++h) {
-                    const int32_t r = sm.tab_row[h][col];
+        __syncthreads();  // folds done: the phase-2 buffers become the output lists
+
+        // ---- phase 4a: merge the P owner tables of each column, sort, drop zeros
+        if (p.want_a) {
+            // owners of a column are adjacent lanes: prefix of nown inside the group
+            int pre = nown;
+#pragma unroll
+            for (int o = 1; o < P; o <<= 1) {
+                const int y2 = __shfl_up_sync(0xffffffffu, pre, o, P);
+                if (u >= o) pre += y2;
+            }
+            const int total = __shfl_sync(0xffffffffu, pre, P - 1, P);
+            pre -= nown;
+            if (mine && total <= T::MAXS) {
+                int q = pre;
+#pragma unroll
+                for (int h = 0; h < T::HSU; ++h) {
+                    const int32_t r = tab_row[h * T::THREADS + tid];
                     if (r < 0) continue;
-                    const double v = sm.tab_acc[h][col];
-                    const double tv = sm.tab_tacc[h][col];
-                    int q = n++;
-                    while (q > 0 && sm.u.out.a_row[q - 1][col] > r) {
-                        sm.u.out.a_row[q][col] = sm.u.out.a_row[q - 1][col];
-                        sm.u.out.a_val[q][col] = sm.u.out.a_val[q - 1][col];
-                        sm.u.out.f_val[q][col] = sm.u.out.f_val[q - 1][col];
+                    o_row[q * TC + col] = r;
+                    o_val[q * TC + col] = tab_acc[h * T::THREADS + tid];
+                    o_tv[q * TC + col] = LIFT ? tab_tacc[h * T::THREADS + tid] : 0.0;
+                    ++q;
+                }
+            }
+            if (mine && u == 0 && total > T::MAXS) misc[3] = 1;
+            __syncwarp();
+            if (mine && u == 0) {
+                const int n = total <= T::MAXS ? total : 0;
+                for (int a = 1; a < n; ++a) {  // insertion sort by row
+                    const int32_t r = o_row[a * TC + col];
+                    const double v = o_val[a * TC + col];
+                    const double tv = o_tv[a * TC + col];
+                    int q = a;
+                    while (q > 0 && o_row[(q - 1) * TC + col] > r) {
+                        o_row[q * TC + col] = o_row[(q - 1) * TC + col];
+                        o_val[q * TC + col] = o_val[(q - 1) * TC + col];
+                        o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
                         --q;
                     }
-                    sm.u.out.a_row[q][col] = r;
-                    sm.u.out.a_val[q][col] = v;
-                    sm.u.out.f_val[q][col] = tv;  // transposed value (lift), parked
+                    o_row[q * TC + col] = r;
+                    o_val[q * TC + col] = v;
+                    o_tv[q * TC + col] = tv;
                 }
-            }
-            // Dirichlet lift: (A u0)[c] = sum over stored A(c, r) in ascending r
-            if (p.need_lift) {
+                // Dirichlet lift: (A u0)[c] = sum over stored A(c, r), ascending r
+                if (LIFT)
+                    for (int q = 0; q < n; ++q) {
+                        const int32_t r = o_row[q * TC + col];
+                        const double a_cr = o_tv[q * TC + col];
+                        if (a_cr != 0.0 && p.is_dir[r]) {
+                            const double uu = node_field(p.g_dir, p.nodes, D, r);
+                            if (uu != 0.0) y = y + a_cr * uu;
+                        }
+                    }
+                const bool col_free = p.want_sys && p.fidx[c] >= 0;
+                int ka = 0, kf = 0;
                 for (int q = 0; q < n; ++q) {
-                    const int32_t r = sm.u.out.a_row[q][col];
-                    const double a_cr = sm.u.out.f_val[q][col];
-                    if (a_cr != 0.0 && p.is_dir[r]) {
-                        const double u = node_field(p.g_dir, p.nodes, D, r);
-                        if (u != 0.0) y = y + a_cr * u;
+                    const int32_t r = o_row[q * TC + col];
+                    const double v = o_val[q * TC + col];
+                    if (v == 0.0) continue;  // sparse.hpp:105
+                    o_row[ka * TC + col] = r;
+                    o_val[ka * TC + col] = v;
+                    ++ka;
+                    if (col_free) {
+                        const int32_t fr = p.fidx[r];
+                        if (fr >= 0) {
+                            f_row[kf * TC + col] = fr;
+                            f_val[kf * TC + col] = v;
+                            ++kf;
+                        }
                     }
                 }
+                na[col] = ka;
+                nf[col] = kf;
             }
-            // zero drop (sparse.hpp:105); A(free, free) keeps free rows of free columns
-            const bool col_free = p.want_sys && p.fidx[c] >= 0;
-            int na = 0, nf = 0;
-            for (int q = 0; q < n; ++q) {
-                const int32_t r = sm.u.out.a_row[q][col];
-                const double v = sm.u.out.a_val[q][col];
-                if (v == 0.0) continue;
-                sm.u.out.a_row[na][col] = r;
-                sm.u.out.a_val[na][col] = v;
-                ++na;
-                if (col_free) {
-                    const int32_t fr = p.fidx[r];
-                    if (fr >= 0) {
-                        sm.u.out.f_row[nf][col] = fr;
-                        sm.u.out.f_val[nf][col] = v;
-                        ++nf;
-                    }
+        }
+        if (tid < TC && (tid >= ncols || !p.want_a)) na[tid] = nf[tid] = 0;
+        __syncthreads();
+
+        // ---- phase 4b: tile prefix, look-back, coalesced writes
+        if (tid < 32) {
+            constexpr int PER = (TC + 31) / 32;  // columns per lane
+            int va[PER], vf[PER], sa = 0, sf = 0;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int q = tid * PER + e;
+                va[e] = q < TC ? na[q] : 0;
+                vf[e] = q < TC ? nf[q] : 0;
+                sa += va[e];
+                sf += vf[e];
+            }
+            int ia = sa, iff = sf;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ya = __shfl_up_sync(0xffffffffu, ia, o);
+                const int yf = __shfl_up_sync(0xffffffffu, iff, o);
+                if (tid >= o) {
+                    ia += ya;
+                    iff += yf;
                 }
             }
-            sm.na[col] = na;
-            sm.nf[col] = nf;
-        } else if (tid < T::TC) {
-            sm.na[tid] = sm.nf[tid] = 0;
-        }
-        __syncthreads();
-        // ---- phase 4: tile prefix, look-back, coalesced writes
-        if (tid == 0) {
-            int32_t ra = 0, rf = 0;
-            for (int q = 0; q < T::TC; ++q) {
-                const int32_t a = sm.na[q], f = sm.nf[q];
-                sm.na[q] = ra;
-                sm.nf[q] = rf;
-                ra += a;
-                rf += f;
+            const int ta = __shfl_sync(0xffffffffu, ia, 31);
+            const int tf = __shfl_sync(0xffffffffu, iff, 31);
+            int ea = ia - sa, ef = iff - sf;
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int q = tid * PER + e;
+                if (q < TC) {
+                    na[q] = ea;
+                    nf[q] = ef;
+                }
+                ea += va[e];
+                ef += vf[e];
             }
-            sm.na[T::TC] = ra;
-            sm.nf[T::TC] = rf;
-            if (sm.bad) atomicOr(p.err, DERR_V2_OVERFLOW);
-            const uint64_t ex = lookback(p.tile_status, tile, ((uint64_t)rf << 31) | (uint64_t)ra);
-            sm.off_a = (int64_t)(ex & 0x7FFFFFFFull);
-            sm.off_f = (int64_t)(ex >> 31);
+            if (tid == 0) {
+                na[TC] = ta;
+                nf[TC] = tf;
+            }
+            const uint64_t ex =
+                warp_lookback(p.tile_status, tile, ((uint64_t)tf << 31) | (uint64_t)ta);
+            if (tid == 0) {
+                misc[1] = (int64_t)(ex & 0x7FFFFFFFull);
+                misc[2] = (int64_t)(ex >> 31);
+                if (misc[3]) atomicOr(p.err, DERR_V2_OVERFLOW);
+            }
         }
         __syncthreads();
-        const int64_t off_a = sm.off_a, off_f = sm.off_f;
-        const int ta = sm.na[T::TC], tf = sm.nf[T::TC];
+        const int64_t off_a = misc[1], off_f = misc[2];
+        const int ta = na[TC], tf = nf[TC];
         if (p.want_a) {
-            if (off_a + ta > p.cap_a || off_f + tf > p.cap_ff) {
+            if (off_a + ta > p.cap_a || (p.want_sys && off_f + tf > p.cap_ff)) {
                 if (tid == 0) atomicOr(p.err, DERR_CAPACITY);
             } else {
                 for (int e = tid; e < ta; e += T::THREADS) {
-                    int lo = 0, hi = T::TC;  // column of entry e
+                    int lo = 0, hi = TC;  // last column whose prefix <= e
+#pragma unroll 1
                     while (hi - lo > 1) {
                         const int mid = (lo + hi) >> 1;
-                        if (sm.na[mid] <= e) lo = mid;
+                        if (na[mid] <= e) lo = mid;
                         else hi = mid;
                     }
-                    while (lo + 1 < T::TC && sm.na[lo + 1] <= e) ++lo;
-                    const int q = e - sm.na[lo];
-                    p.row_idx[off_a + e] = sm.u.out.a_row[q][lo];
-                    p.values[off_a + e] = sm.u.out.a_val[q][lo];
+                    const int q = e - na[lo];
+                    p.row_idx[off_a + e] = o_row[q * TC + lo];
+                    p.values[off_a + e] = o_val[q * TC + lo];
                 }
                 if (p.want_sys)
                     for (int e = tid; e < tf; e += T::THREADS) {
-                        int lo = 0, hi = T::TC;
+                        int lo = 0, hi = TC;
+#pragma unroll 1
                         while (hi - lo > 1) {
                             const int mid = (lo + hi) >> 1;
-                            if (sm.nf[mid] <= e) lo = mid;
+                            if (nf[mid] <= e) lo = mid;
                             else hi = mid;
                         }
-                        while (lo + 1 < T::TC && sm.nf[lo + 1] <= e) ++lo;
-                        const int q = e - sm.nf[lo];
-                        p.ff_row_idx[off_f + e] = sm.u.out.f_row[q][lo];
-                        p.ff_values[off_f + e] = sm.u.out.f_val[q][lo];
+                        const int q = e - nf[lo];
+                        p.ff_row_idx[off_f + e] = f_row[q * TC + lo];
+                        p.ff_values[off_f + e] = f_val[q * TC + lo];
                     }
-                if (mine) {
-                    p.col_ptr[c + 1] = (int32_t)(off_a + sm.na[col + 1]);
-                }
+                if (mine && u == 0) p.col_ptr[c + 1] = (int32_t)(off_a + na[col + 1]);
             }
         }
-        if (mine) {
+        if (mine && u == 0) {
             if (p.want_b) p.b[c] = b;
             if (p.want_sys) {
-                const bool dir = p.is_dir[c];
-                const double u0 = dir ? node_field(p.g_dir, p.nodes, D, c) : 0.0;
-                const double bmod = p.need_lift ? b - y : b - 0.0;
+                const double u0 = p.is_dir[c] ? node_field(p.g_dir, p.nodes, D, c) : 0.0;
+                const double bmod = LIFT ? b - y : b - 0.0;
                 p.u0[c] = u0;
                 p.b_mod[c] = bmod;
                 const int32_t fc = p.fidx[c];
                 if (fc >= 0) {
                     p.b_f[fc] = bmod;
-                    if (p.want_a) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + sm.nf[col + 1]);
+                    if (p.want_a) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + nf[col + 1]);
                 }
             }
         }
@@ -417,34 +492,33 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
     }
 }
 
-int launch_columns2(fl_ctx* ctx, int dim, ColParams& p) {
-    if (dim == 2) {
-        const size_t smem = sizeof(TileSmem<2>);
-        p.n_tiles = (p.n_nodes + Tile<2>::TC - 1) / Tile<2>::TC;
-        FL_CUDA(cudaFuncSetAttribute(k_columns2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns2<2>, Tile<2>::THREADS, smem);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-        k_columns2<2><<<grid, Tile<2>::THREADS, smem, ctx->stream>>>(p);
-    } else {
-        const size_t smem = sizeof(TileSmem<3>);
-        p.n_tiles = (p.n_nodes + Tile<3>::TC - 1) / Tile<3>::TC;
-        FL_CUDA(cudaFuncSetAttribute(k_columns2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns2<3>, Tile<3>::THREADS, smem);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-        k_columns2<3><<<grid, Tile<3>::THREADS, smem, ctx->stream>>>(p);
-    }
+template <int D, int KMAX, bool LIFT>
+static int launch_variant(fl_ctx* ctx, ColParams& p) {
+    using LY = Layout<D, KMAX, LIFT>;
+    const size_t smem = LY::BYTES;
+    auto kern = k_columns2<D, KMAX, LIFT>;
+    FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tile<D>::THREADS, smem));
+    p.n_tiles = (p.n_nodes + Tile<D>::TC - 1) / Tile<D>::TC;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    kern<<<(int)grid, Tile<D>::THREADS, smem, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;
 }
 
-int64_t columns2_tiles(int dim, int32_t n_nodes) {
-    const int tc = dim == 2 ? Tile<2>::TC : Tile<3>::TC;
-    return (n_nodes + tc - 1) / tc;
+// kmax: the plan's largest node valence (incidences per node)
+int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax) {
+    if (dim == 2) {
+        if (kmax <= 8)
+            return p.need_lift ? launch_variant<2, 8, true>(ctx, p) : launch_variant<2, 8, false>(ctx, p);
+        return p.need_lift ? launch_variant<2, 16, true>(ctx, p) : launch_variant<2, 16, false>(ctx, p);
+    }
+    if (kmax <= 24)
+        return p.need_lift ? launch_variant<3, 24, true>(ctx, p) : launch_variant<3, 24, false>(ctx, p);
+    return p.need_lift ? launch_variant<3, 32, true>(ctx, p) : launch_variant<3, 32, false>(ctx, p);
 }
 
 }  // namespace fl

@@ -610,14 +610,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
             s_nf[w] = p.want_a && has ? ws.n_ff : 0;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < 32) {
             uint64_t agg_a = 0, agg_f = 0;
             for (int q = 0; q < kWarps; ++q) {
                 agg_a += (uint64_t)s_na[q];
                 agg_f += (uint64_t)s_nf[q];
             }
             // packed [61:31] = A(free,free) count, [30:0] = A count
-            s_off = lookback(p.tile_status, tile, (agg_f << 31) | agg_a);
+            const uint64_t e = warp_lookback(p.tile_status, tile, (agg_f << 31) | agg_a);
+            if (threadIdx.x == 0) s_off = e;
         }
         __syncthreads();
         if (has) {

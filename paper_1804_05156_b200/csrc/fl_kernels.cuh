@@ -47,7 +47,7 @@ int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
                      int32_t* row_map, int32_t* cnt, uint32_t* d_err, int64_t* nnz_out);
 int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
                         double* qi);
-int launch_columns2(fl_ctx* ctx, int dim, ColParams& p);
+int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
 size_t column_smem_bytes();
 int column_tile_width();

@@ -48,6 +48,41 @@ __device__ __forceinline__ uint64_t lookback(uint64_t* status, int64_t tile, uin
     return excl;
 }
 
+// Warp-wide variant (call with all 32 lanes of ONE warp; every lane returns the
+// exclusive prefix).  Each round inspects 32 predecessors at once: the walk over
+// tiles that have only published aggregates costs one L2 round trip per 32
+// tiles instead of one per tile.
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t* status, int64_t tile,
+                                                  uint64_t aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_status(&status[0], kFlagInc | aggregate);
+        return 0;
+    }
+    if (lane == 0) st_status(&status[tile], kFlagAgg | aggregate);
+    uint64_t excl = 0;
+    int64_t hi = tile - 1;  // window covers predecessors hi, hi-1, ..., hi-31
+    while (true) {
+        const int64_t idx = hi - lane;
+        uint64_t v = idx >= 0 ? ld_status(&status[idx]) : (kFlagInc | 0ull);
+        uint32_t flag = (uint32_t)(v >> 62);
+        // the nearest inclusive prefix in the window
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, flag == 2);
+        const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+        // lanes up to the inclusive one must all have published something
+        const unsigned empty = __ballot_sync(0xffffffffu, flag == 0 && lane <= first_inc);
+        if (empty) continue;  // re-read the same window
+        uint64_t part = (lane <= first_inc) ? (v & kValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (first_inc < 32) break;
+        hi -= 32;
+    }
+    if (lane == 0) st_status(&status[tile], kFlagInc | (excl + aggregate));
+    return excl;
+}
+
 template <int BLOCK>
 __device__ __forceinline__ int64_t block_exclusive_sum(int64_t x, int64_t* warp_sums,
                                                        int64_t& total) {
@@ -96,7 +131,10 @@ __global__ void __launch_bounds__(BLOCK) k_scan(int64_t n, F f, OutT* out, uint6
     }
     int64_t total;
     int64_t excl = block_exclusive_sum<BLOCK>(local, warp_sums, total);
-    if (threadIdx.x == 0) s_excl = (int64_t)lookback(status, tile, (uint64_t)total);
+    if (threadIdx.x < 32) {
+        const uint64_t e = warp_lookback(status, tile, (uint64_t)total);
+        if (threadIdx.x == 0) s_excl = (int64_t)e;
+    }
     __syncthreads();
     excl += s_excl;
 #pragma unroll
