@@ -41,16 +41,16 @@ template <>
 struct Tile<2> {
     static constexpr int TC = 64;       // columns per tile
     static constexpr int THREADS = 128;
-    static constexpr int HSU = 8;       // slot table entries per (column, owner thread)
-    static constexpr int MAXU = 6;      // distinct rows per owner thread (load 0.75)
-    static constexpr int MAXS = 12;     // distinct rows per column
+    static constexpr int HSU = 16;      // slot table entries per column
+    static constexpr int MAXU = 12;     // distinct rows per column (load 0.75)
+    static constexpr int MAXS = 12;
 };
 template <>
 struct Tile<3> {
     static constexpr int TC = 32;
     static constexpr int THREADS = 128;
-    static constexpr int HSU = 8;
-    static constexpr int MAXU = 6;
+    static constexpr int HSU = 32;
+    static constexpr int MAXU = 24;
     static constexpr int MAXS = 24;
 };
 
@@ -59,7 +59,7 @@ struct Layout {
     using T = Tile<D>;
     static constexpr int NV = D + 1;
     static constexpr int TC = T::TC;
-    static constexpr int P = T::THREADS / T::TC;  // threads per column
+    static constexpr int P = 1;                   // fold threads per column
     static constexpr int SROW = NV * TC + 1;      // padded stride of one rank row
     static constexpr int LROW = TC + 1;
     // byte offsets of the dynamic smem carve-up
@@ -77,10 +77,10 @@ struct Layout {
     static constexpr size_t OUT_END = F_VAL + sizeof(double) * T::MAXS * TC;
     static constexpr size_t UNION_END = IN_END > OUT_END ? IN_END : OUT_END;
     static constexpr size_t KEY_OFF = (UNION_END + 15) & ~size_t(15);           // uint32 [TC*KMAX]
-    static constexpr size_t TR_OFF = KEY_OFF + sizeof(uint32_t) * TC * KMAX;    // int32 [HSU][THREADS]
-    static constexpr size_t TA_OFF = TR_OFF + sizeof(int32_t) * T::HSU * T::THREADS;  // double
-    static constexpr size_t TT_OFF = TA_OFF + sizeof(double) * T::HSU * T::THREADS;   // double (LIFT)
-    static constexpr size_t TAB_END = TT_OFF + (LIFT ? sizeof(double) * T::HSU * T::THREADS : 0);
+    static constexpr size_t TR_OFF = KEY_OFF + sizeof(uint32_t) * TC * KMAX;    // int32 [HSU][TC]
+    static constexpr size_t TA_OFF = TR_OFF + sizeof(int32_t) * T::HSU * TC;    // double
+    static constexpr size_t TT_OFF = TA_OFF + sizeof(double) * T::HSU * TC;     // double (LIFT)
+    static constexpr size_t TAB_END = TT_OFF + (LIFT ? sizeof(double) * T::HSU * TC : 0);
     static constexpr size_t PTR_OFF = TAB_END;                                   // int32 [TC+1]
     static constexpr size_t NA_OFF = PTR_OFF + sizeof(int32_t) * (TC + 1);      // int32 [TC+1]
     static constexpr size_t NF_OFF = NA_OFF + sizeof(int32_t) * (TC + 1);       // int32 [TC+1]
@@ -221,27 +221,38 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
         double b = 0.0, y = 0.0;
         int nown = 0;
         if (mine && p.want_a) {
+            const int32_t* __restrict__ Rc = R + col;
+            const double* __restrict__ Sc = S + col;
+            int32_t* __restrict__ trow = tab_row + col;
+            double* __restrict__ tacc = tab_acc + col;
 #pragma unroll
-            for (int h = 0; h < T::HSU; ++h) tab_row[h * T::THREADS + tid] = -1;
+            for (int h = 0; h < T::HSU; ++h) trow[h * TC] = -1;
             bool over = false;
             for (int i = 0; i < NV; ++i) {
+                // software pipeline: the next item's row/value are loaded before
+                // the current accumulator update
+                int32_t r_nx = m > 0 ? Rc[i * TC] : 0;
+                double s_nx = m > 0 ? Sc[i * TC] : 0.0;
                 for (int k = 0; k < m; ++k) {
-                    const int32_t r = R[k * LY::SROW + i * TC + col];
-                    const uint32_t hv = (uint32_t)r * 2654435761u;
-                    if (P > 1 && (int)(hv >> (32 - LOGP)) != u) continue;
-                    uint32_t h = (hv >> (32 - LOGP - LOGH)) & (T::HSU - 1);
+                    const int32_t r = r_nx;
+                    const double sv = s_nx;
+                    if (k + 1 < m) {
+                        r_nx = Rc[(k + 1) * LY::SROW + i * TC];
+                        s_nx = Sc[(k + 1) * LY::SROW + i * TC];
+                    }
+                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
                     int slot = -1;
                     while (true) {
-                        const int32_t kk = tab_row[h * T::THREADS + tid];
+                        const int32_t kk = trow[h * TC];
                         if (kk == r) {
                             slot = (int)h;
                             break;
                         }
                         if (kk == -1) {
                             if (nown >= T::MAXU) break;
-                            tab_row[h * T::THREADS + tid] = r;
-                            tab_acc[h * T::THREADS + tid] = -0.0;  // -0.0 + x == x
-                            if (LIFT) tab_tacc[h * T::THREADS + tid] = -0.0;
+                            trow[h * TC] = r;
+                            tacc[h * TC] = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                            if (LIFT) tab_tacc[h * TC + col] = -0.0;
                             ++nown;
                             slot = (int)h;
                             break;
@@ -252,8 +263,7 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
                         over = true;
                         continue;
                     }
-                    double& a = tab_acc[slot * T::THREADS + tid];
-                    a = a + S[k * LY::SROW + i * TC + col];
+                    tacc[slot * TC] = tacc[slot * TC] + sv;
                 }
             }
             if (over) misc[3] = 1;
@@ -268,11 +278,9 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
                     for (int i = 0; i < NV; ++i)
                         for (int k = k0; k < k1; ++k) {
                             const int32_t r = R[k * LY::SROW + i * TC + col];
-                            const uint32_t hv = (uint32_t)r * 2654435761u;
-                            if (P > 1 && (int)(hv >> (32 - LOGP)) != u) continue;
-                            uint32_t h = (hv >> (32 - LOGP - LOGH)) & (T::HSU - 1);
-                            while (tab_row[h * T::THREADS + tid] != r) h = (h + 1) & (T::HSU - 1);
-                            double& a = tab_tacc[h * T::THREADS + tid];
+                            uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
+                            while (tab_row[h * TC + col] != r) h = (h + 1) & (T::HSU - 1);
+                            double& a = tab_tacc[h * TC + col];
                             a = a + S[k * LY::SROW + i * TC + col];
                         }
                     k0 = k1;
@@ -314,48 +322,27 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
         }
         __syncthreads();  // folds done: the phase-2 buffers become the output lists
 
-        // ---- phase 4a: merge the P owner tables of each column, sort, drop zeros
+        // ---- phase 4a: slots -> rows in ascending order, drop exact zeros
         if (p.want_a) {
-            // owners of a column are adjacent lanes: prefix of nown inside the group
-            int pre = nown;
-#pragma unroll
-            for (int o = 1; o < P; o <<= 1) {
-                const int y2 = __shfl_up_sync(0xffffffffu, pre, o, P);
-                if (u >= o) pre += y2;
-            }
-            const int total = __shfl_sync(0xffffffffu, pre, P - 1, P);
-            pre -= nown;
-            if (mine && total <= T::MAXS) {
-                int q = pre;
-#pragma unroll
-                for (int h = 0; h < T::HSU; ++h) {
-                    const int32_t r = tab_row[h * T::THREADS + tid];
+            if (mine) {
+                const int n = nown <= T::MAXS ? nown : 0;
+                // the rows of a column are distinct: rank = number of smaller rows
+                for (int h = 0; h < T::HSU && n > 0; ++h) {
+                    const int32_t r = tab_row[h * TC + col];
                     if (r < 0) continue;
-                    o_row[q * TC + col] = r;
-                    o_val[q * TC + col] = tab_acc[h * T::THREADS + tid];
-                    o_tv[q * TC + col] = LIFT ? tab_tacc[h * T::THREADS + tid] : 0.0;
-                    ++q;
-                }
-            }
-            if (mine && u == 0 && total > T::MAXS) misc[3] = 1;
-            __syncwarp();
-            if (mine && u == 0) {
-                const int n = total <= T::MAXS ? total : 0;
-                for (int a = 1; a < n; ++a) {  // insertion sort by row
-                    const int32_t r = o_row[a * TC + col];
-                    const double v = o_val[a * TC + col];
-                    const double tv = o_tv[a * TC + col];
-                    int q = a;
-                    while (q > 0 && o_row[(q - 1) * TC + col] > r) {
-                        o_row[q * TC + col] = o_row[(q - 1) * TC + col];
-                        o_val[q * TC + col] = o_val[(q - 1) * TC + col];
-                        o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
-                        --q;
+                    int q = 0;
+#pragma unroll 4
+                    for (int h2 = 0; h2 < T::HSU; ++h2) {
+                        const int32_t r2 = tab_row[h2 * TC + col];
+                        q += (r2 >= 0) & (r2 < r);
                     }
                     o_row[q * TC + col] = r;
-                    o_val[q * TC + col] = v;
-                    o_tv[q * TC + col] = tv;
+                    o_val[q * TC + col] = tab_acc[h * TC + col];
+                    o_tv[q * TC + col] = LIFT ? tab_tacc[h * TC + col] : 0.0;
                 }
+            }
+            if (mine) {
+                const int n = nown <= T::MAXS ? nown : 0;
                 // Dirichlet lift: (A u0)[c] = sum over stored A(c, r), ascending r
                 if (LIFT)
                     for (int q = 0; q < n; ++q) {

@@ -12,14 +12,18 @@
 
 namespace fl {
 
-// status word: [63:62] flag (0 empty, 1 aggregate, 2 inclusive prefix), [61:0] value
+// status word: [63:62] flag (0 empty, 1 aggregate, 2 inclusive prefix), [61:0] value.
+// Flag and value travel in ONE 64-bit word, so relaxed (not acquire/release)
+// accesses suffice: no other data is published through it.  ld.acquire.gpu
+// compiles to CCTL.IVALL (a full L1 invalidation per poll) on sm_100a, which
+// wiped every CTA's L1 working set while a tile waited (profiles/ v2 notes).
 __device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
     uint64_t v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 constexpr uint64_t kFlagAgg = 1ull << 62;
