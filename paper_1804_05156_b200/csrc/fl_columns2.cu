@@ -25,6 +25,8 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "fl_geometry.cuh"
 #include "fl_internal.cuh"
@@ -35,28 +37,20 @@ namespace fl {
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
-template <int D>
-struct Tile;
-template <>
-struct Tile<2> {
-    static constexpr int TC = 64;       // columns per tile
-    static constexpr int THREADS = 128;
-    static constexpr int HSU = 16;      // slot table entries per column
-    static constexpr int MAXU = 12;     // distinct rows per column (load 0.75)
-    static constexpr int MAXS = 12;
-};
-template <>
-struct Tile<3> {
-    static constexpr int TC = 32;
-    static constexpr int THREADS = 128;
-    static constexpr int HSU = 32;
-    static constexpr int MAXU = 24;
-    static constexpr int MAXS = 24;
+// Tile shape: TC columns per CTA of THREADS threads; per-column slot table of
+// HSU entries holding at most MAXS distinct rows (load factor 0.75).
+template <int D, int TC_, int THREADS_>
+struct Tile {
+    static constexpr int TC = TC_;
+    static constexpr int THREADS = THREADS_;
+    static constexpr int HSU = D == 2 ? 16 : 32;
+    static constexpr int MAXU = D == 2 ? 12 : 24;
+    static constexpr int MAXS = MAXU;
 };
 
-template <int D, int KMAX, bool LIFT>
+template <class T_, int D, int KMAX, bool LIFT>
 struct Layout {
-    using T = Tile<D>;
+    using T = T_;
     static constexpr int NV = D + 1;
     static constexpr int TC = T::TC;
     static constexpr int P = 1;                   // fold threads per column
@@ -98,10 +92,10 @@ __device__ __forceinline__ double node_field(const FieldDesc& g, const double* n
     return eval_point(g, x, y, z);
 }
 
-template <int D, int KMAX, bool LIFT>
-__global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
-    using T = Tile<D>;
-    using LY = Layout<D, KMAX, LIFT>;
+template <int D, int TCX, int THR, int KMAX, bool LIFT>
+__global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
+    using T = Tile<D, TCX, THR>;
+    using LY = Layout<T, D, KMAX, LIFT>;
     constexpr int NV = D + 1;
     constexpr int TC = T::TC;
     constexpr int P = LY::P;
@@ -324,21 +318,26 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
 
         // ---- phase 4a: slots -> rows in ascending order, drop exact zeros
         if (p.want_a) {
-            if (mine) {
-                const int n = nown <= T::MAXS ? nown : 0;
-                // the rows of a column are distinct: rank = number of smaller rows
-                for (int h = 0; h < T::HSU && n > 0; ++h) {
+            if (mine && nown <= T::MAXS) {
+                // extract the slots with an insertion sort by row
+                int n = 0;
+                for (int h = 0; h < T::HSU; ++h) {
                     const int32_t r = tab_row[h * TC + col];
                     if (r < 0) continue;
-                    int q = 0;
-#pragma unroll 4
-                    for (int h2 = 0; h2 < T::HSU; ++h2) {
-                        const int32_t r2 = tab_row[h2 * TC + col];
-                        q += (r2 >= 0) & (r2 < r);
+                    const double v = tab_acc[h * TC + col];
+                    const double tv = LIFT ? tab_tacc[h * TC + col] : 0.0;
+                    int q = n++;
+                    while (q > 0) {
+                        const int32_t rp = o_row[(q - 1) * TC + col];
+                        if (rp < r) break;
+                        o_row[q * TC + col] = rp;
+                        o_val[q * TC + col] = o_val[(q - 1) * TC + col];
+                        if (LIFT) o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
+                        --q;
                     }
                     o_row[q * TC + col] = r;
-                    o_val[q * TC + col] = tab_acc[h * TC + col];
-                    o_tv[q * TC + col] = LIFT ? tab_tacc[h * TC + col] : 0.0;
+                    o_val[q * TC + col] = v;
+                    if (LIFT) o_tv[q * TC + col] = tv;
                 }
             }
             if (mine) {
@@ -479,33 +478,48 @@ __global__ void __launch_bounds__(Tile<D>::THREADS) k_columns2(ColParams p) {
     }
 }
 
-template <int D, int KMAX, bool LIFT>
+template <int D, int TCX, int THR, int KMAX, bool LIFT>
 static int launch_variant(fl_ctx* ctx, ColParams& p) {
-    using LY = Layout<D, KMAX, LIFT>;
+    using T = Tile<D, TCX, THR>;
+    using LY = Layout<T, D, KMAX, LIFT>;
     const size_t smem = LY::BYTES;
-    auto kern = k_columns2<D, KMAX, LIFT>;
+    auto kern = k_columns2<D, TCX, THR, KMAX, LIFT>;
     FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tile<D>::THREADS, smem));
-    p.n_tiles = (p.n_nodes + Tile<D>::TC - 1) / Tile<D>::TC;
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THR, smem));
+    p.n_tiles = (p.n_nodes + TCX - 1) / TCX;
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    kern<<<(int)grid, Tile<D>::THREADS, smem, ctx->stream>>>(p);
+    kern<<<(int)grid, THR, smem, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;
 }
 
-// kmax: the plan's largest node valence (incidences per node)
+template <int D, int TCX, int THR>
+static int launch_shape(fl_ctx* ctx, ColParams& p, int kmax) {
+    constexpr int K_SMALL = D == 2 ? 8 : 24, K_LARGE = D == 2 ? 16 : 32;
+    if (kmax <= K_SMALL)
+        return p.need_lift ? launch_variant<D, TCX, THR, K_SMALL, true>(ctx, p)
+                           : launch_variant<D, TCX, THR, K_SMALL, false>(ctx, p);
+    return p.need_lift ? launch_variant<D, TCX, THR, K_LARGE, true>(ctx, p)
+                       : launch_variant<D, TCX, THR, K_LARGE, false>(ctx, p);
+}
+
+// kmax: the plan's largest node valence (incidences per node).  FL_TILE=<TC>x<THREADS>
+// selects an alternative tile shape (tuning experiments).
 int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax) {
+    const char* env = std::getenv("FL_TILE");
+    const std::string shape = env ? env : "";
     if (dim == 2) {
-        if (kmax <= 8)
-            return p.need_lift ? launch_variant<2, 8, true>(ctx, p) : launch_variant<2, 8, false>(ctx, p);
-        return p.need_lift ? launch_variant<2, 16, true>(ctx, p) : launch_variant<2, 16, false>(ctx, p);
+        if (shape == "32x64") return launch_shape<2, 32, 64>(ctx, p, kmax);
+        if (shape == "32x128") return launch_shape<2, 32, 128>(ctx, p, kmax);
+        return launch_shape<2, 64, 128>(ctx, p, kmax);
     }
-    if (kmax <= 24)
-        return p.need_lift ? launch_variant<3, 24, true>(ctx, p) : launch_variant<3, 24, false>(ctx, p);
-    return p.need_lift ? launch_variant<3, 32, true>(ctx, p) : launch_variant<3, 32, false>(ctx, p);
+    if (shape == "16x64") return launch_shape<3, 16, 64>(ctx, p, kmax);
+    if (shape == "16x128") return launch_shape<3, 16, 128>(ctx, p, kmax);
+    if (shape == "32x64") return launch_shape<3, 32, 64>(ctx, p, kmax);
+    return launch_shape<3, 32, 128>(ctx, p, kmax);
 }
 
 }  // namespace fl
