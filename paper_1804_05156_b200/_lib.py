@@ -51,6 +51,7 @@ SIGNATURES = {
     "fl_launch_count": (C.c_int64, [_vp]),
     "fl_last_timings": (C.c_int, [_vp, _vp]),
     "fl_selftest_div": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_int]),
+    "fl_phase_cycles": (C.c_int, [_vp, _vp]),
     "fl_host_sample": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _vp, _vp, C.c_int, C.c_int,
                                  C.c_double, _vp]),
 }

@@ -168,6 +168,9 @@ FL_API int fl_create(int device, fl_ctx** out) {
     ctx->profile = prof && prof[0] == '1';
     if (ctx->profile)
         for (auto& ev : ctx->ev) FL_CUDA(cudaEventCreate(&ev));
+    const char* ph = std::getenv("FL_PHASES");
+    ctx->phase_timing = ph && ph[0] == '1';
+    if (ctx->phase_timing) FL_TRY(ctx->phases.ensure(sizeof(unsigned long long) * 8));
     *out = ctx;
     return FL_OK;
 }
@@ -473,6 +476,11 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         p.err = counters + CNT_ERR;
         p.cap_a = want_a ? (int64_t)cap : 0;
         p.cap_ff = want_sys ? (int64_t)cap : 0;
+        p.phase_cycles = nullptr;
+        if (ctx->phase_timing) {
+            p.phase_cycles = ctx->phases.as<unsigned long long>();
+            FL_CUDA(cudaMemsetAsync(p.phase_cycles, 0, sizeof(unsigned long long) * 8, s));
+        }
         x->last = p;
         x->last_mesh = mesh;
         x->last_valid = true;
@@ -653,6 +661,17 @@ FL_API int fl_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_pt
     res->sizes.n = n_cols;
     res->sizes.nnz = nnz;
     res->sizes_valid = true;
+    return FL_OK;
+}
+
+FL_API int fl_phase_cycles(fl_ctx* ctx, uint64_t* out6) {
+    if (!ctx || !out6) return set_error(FL_ERR_ARGUMENT, "null argument");
+    for (int i = 0; i < 6; ++i) out6[i] = 0;
+    if (!ctx->phase_timing) return FL_OK;
+    FL_CUDA(cudaMemcpyAsync(ctx->pinned, ctx->phases.p, sizeof(unsigned long long) * 6,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    FL_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 6; ++i) out6[i] = static_cast<const unsigned long long*>(ctx->pinned)[i];
     return FL_OK;
 }
 

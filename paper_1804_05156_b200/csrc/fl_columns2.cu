@@ -126,12 +126,24 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
     // phase-3 identity: column `col`, owner slot `u`
     const int col = tid >> LOGP;
     const int u = tid & (P - 1);
+    long long ph_t = 0, ph_acc[6] = {0, 0, 0, 0, 0, 0};
+#define FL_MARK(k)                                              \
+    if (p.phase_cycles && tid == 0) {                           \
+        const long long now_ = clock64();                       \
+        ph_acc[k] += now_ - ph_t;                               \
+        ph_t = now_;                                            \
+    }
 
     while (true) {
         if (tid == 0) misc[0] = atomicAdd(p.ticket, 1u);
         __syncthreads();
         const int64_t tile = misc[0];
-        if (tile >= p.n_tiles) break;
+        if (tile >= p.n_tiles) {
+            if (p.phase_cycles && tid == 0)
+                for (int q = 0; q < 6; ++q) atomicAdd(p.phase_cycles + q, (unsigned long long)ph_acc[q]);
+            break;
+        }
+        if (p.phase_cycles && tid == 0) ph_t = clock64();
         const int32_t c0 = (int32_t)(tile * TC);
         const int ncols = min(TC, p.n_nodes - c0);
 
@@ -152,6 +164,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         for (int q = tid; q < M; q += T::THREADS) key[q] = __ldg(p.inc + base + q);
         __syncthreads();
 
+        FL_MARK(0)
         // ---- phase 2: rank + geometry, lane per incidence
         for (int q = tid; q < M; q += T::THREADS) {
             const uint32_t kq = key[q];
@@ -208,6 +221,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         }
         __syncthreads();
 
+        FL_MARK(1)
         // ---- phase 3: folds, P threads per column
         const bool mine = col < ncols;
         const int32_t c = c0 + col;
@@ -315,6 +329,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             }
         }
         __syncthreads();  // folds done: the phase-2 buffers become the output lists
+        FL_MARK(2)
 
         // ---- phase 4a: slots -> rows in ascending order, drop exact zeros
         if (p.want_a) {
@@ -377,6 +392,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         if (tid < TC && (tid >= ncols || !p.want_a)) na[tid] = nf[tid] = 0;
         __syncthreads();
 
+        FL_MARK(3)
         // ---- phase 4b: tile prefix, look-back, coalesced writes
         if (tid < 32) {
             constexpr int PER = (TC + 31) / 32;  // columns per lane
@@ -426,6 +442,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             }
         }
         __syncthreads();
+        FL_MARK(4)
         const int64_t off_a = misc[1], off_f = misc[2];
         const int ta = na[TC], tf = nf[TC];
         if (p.want_a) {
@@ -475,8 +492,10 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             }
         }
         __syncthreads();
+        FL_MARK(5)
     }
 }
+
 
 template <int D, int TCX, int THR, int KMAX, bool LIFT>
 static int launch_variant(fl_ctx* ctx, ColParams& p) {

@@ -35,6 +35,7 @@ struct ColParams {
     unsigned int* ticket;
     uint32_t* err;
     int64_t cap_a, cap_ff;
+    unsigned long long* phase_cycles;  // diagnostics: per-phase SM cycles (nullptr = off)
 };
 
 int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);
