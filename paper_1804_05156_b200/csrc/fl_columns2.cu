@@ -75,7 +75,8 @@ struct Layout {
     static constexpr size_t TA_OFF = TR_OFF + sizeof(int32_t) * T::HSU * TC;    // double
     static constexpr size_t TT_OFF = TA_OFF + sizeof(double) * T::HSU * TC;     // double (LIFT)
     static constexpr size_t TAB_END = TT_OFF + (LIFT ? sizeof(double) * T::HSU * TC : 0);
-    static constexpr size_t PTR_OFF = TAB_END;                                   // int32 [TC+1]
+    static constexpr size_t TF_OFF = TAB_END;                                    // int32 [HSU][TC]
+    static constexpr size_t PTR_OFF = TF_OFF + sizeof(int32_t) * T::HSU * TC;   // int32 [TC+1]
     static constexpr size_t NA_OFF = PTR_OFF + sizeof(int32_t) * (TC + 1);      // int32 [TC+1]
     static constexpr size_t NF_OFF = NA_OFF + sizeof(int32_t) * (TC + 1);       // int32 [TC+1]
     static constexpr size_t MISC_OFF = (NF_OFF + sizeof(int32_t) * (TC + 1) + 15) & ~size_t(15);
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
     int32_t* tab_row = reinterpret_cast<int32_t*>(smem + LY::TR_OFF);
     double* tab_acc = reinterpret_cast<double*>(smem + LY::TA_OFF);
     double* tab_tacc = reinterpret_cast<double*>(smem + LY::TT_OFF);
+    int32_t* tab_fidx = reinterpret_cast<int32_t*>(smem + LY::TF_OFF);
     int32_t* ptr = reinterpret_cast<int32_t*>(smem + LY::PTR_OFF);
     int32_t* na = reinterpret_cast<int32_t*>(smem + LY::NA_OFF);
     int32_t* nf = reinterpret_cast<int32_t*>(smem + LY::NF_OFF);
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
 
         // ---- phase 1: the tile's incidence keys
         const int32_t base = __ldg(p.inc_ptr + c0);
-        if (tid <= TC) ptr[tid] = __ldg(p.inc_ptr + c0 + min(tid, ncols)) - base;
+        for (int q = tid; q <= TC; q += T::THREADS) ptr[q] = __ldg(p.inc_ptr + c0 + min(q, ncols)) - base;
         if (tid == 0) misc[3] = 0;
         __syncthreads();
         const int M = ptr[ncols];
@@ -329,6 +331,14 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             }
         }
         __syncthreads();  // folds done: the phase-2 buffers become the output lists
+        // free ranks of every slot row, gathered by all threads at once (the
+        // zero-drop loop below would otherwise wait on one gather per entry)
+        if (p.want_sys && p.want_a)
+            for (int e = tid; e < T::HSU * TC; e += T::THREADS) {
+                const int32_t r = tab_row[e];
+                if (r >= 0 && (e % TC) < ncols) tab_fidx[e] = __ldg(p.fidx + r);
+            }
+        __syncthreads();
         FL_MARK(2)
 
         // ---- phase 4a: slots -> rows in ascending order, drop exact zeros
@@ -341,17 +351,20 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                     if (r < 0) continue;
                     const double v = tab_acc[h * TC + col];
                     const double tv = LIFT ? tab_tacc[h * TC + col] : 0.0;
+                    const int32_t fx = p.want_sys ? tab_fidx[h * TC + col] : -1;
                     int q = n++;
                     while (q > 0) {
                         const int32_t rp = o_row[(q - 1) * TC + col];
                         if (rp < r) break;
                         o_row[q * TC + col] = rp;
                         o_val[q * TC + col] = o_val[(q - 1) * TC + col];
+                        f_row[q * TC + col] = f_row[(q - 1) * TC + col];
                         if (LIFT) o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
                         --q;
                     }
                     o_row[q * TC + col] = r;
                     o_val[q * TC + col] = v;
+                    f_row[q * TC + col] = fx;  // free rank of the row (-1: Dirichlet)
                     if (LIFT) o_tv[q * TC + col] = tv;
                 }
             }
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                     for (int q = 0; q < n; ++q) {
                         const int32_t r = o_row[q * TC + col];
                         const double a_cr = o_tv[q * TC + col];
-                        if (a_cr != 0.0 && p.is_dir[r]) {
+                        if (a_cr != 0.0 && f_row[q * TC + col] < 0) {
                             const double uu = node_field(p.g_dir, p.nodes, D, r);
                             if (uu != 0.0) y = y + a_cr * uu;
                         }
@@ -372,12 +385,12 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                 for (int q = 0; q < n; ++q) {
                     const int32_t r = o_row[q * TC + col];
                     const double v = o_val[q * TC + col];
+                    const int32_t fr = f_row[q * TC + col];
                     if (v == 0.0) continue;  // sparse.hpp:105
                     o_row[ka * TC + col] = r;
                     o_val[ka * TC + col] = v;
                     ++ka;
                     if (col_free) {
-                        const int32_t fr = p.fidx[r];
                         if (fr >= 0) {
                             f_row[kf * TC + col] = fr;
                             f_val[kf * TC + col] = v;
@@ -389,7 +402,8 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                 nf[col] = kf;
             }
         }
-        if (tid < TC && (tid >= ncols || !p.want_a)) na[tid] = nf[tid] = 0;
+        for (int q = tid; q < TC; q += T::THREADS)
+            if (q >= ncols || !p.want_a) na[q] = nf[q] = 0;
         __syncthreads();
 
         FL_MARK(3)
@@ -449,31 +463,23 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             if (off_a + ta > p.cap_a || (p.want_sys && off_f + tf > p.cap_ff)) {
                 if (tid == 0) atomicOr(p.err, DERR_CAPACITY);
             } else {
-                for (int e = tid; e < ta; e += T::THREADS) {
-                    int lo = 0, hi = TC;  // last column whose prefix <= e
-#pragma unroll 1
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (na[mid] <= e) lo = mid;
-                        else hi = mid;
+                // a warp per column: each column's entries are one contiguous run
+                constexpr int NW = T::THREADS / 32;
+                const int lane = tid & 31, wid = tid >> 5;
+                for (int cc = wid; cc < ncols; cc += NW) {
+                    const int b0 = na[cc], n = na[cc + 1] - b0;
+                    for (int q = lane; q < n; q += 32) {
+                        p.row_idx[off_a + b0 + q] = o_row[q * TC + cc];
+                        p.values[off_a + b0 + q] = o_val[q * TC + cc];
                     }
-                    const int q = e - na[lo];
-                    p.row_idx[off_a + e] = o_row[q * TC + lo];
-                    p.values[off_a + e] = o_val[q * TC + lo];
-                }
-                if (p.want_sys)
-                    for (int e = tid; e < tf; e += T::THREADS) {
-                        int lo = 0, hi = TC;
-#pragma unroll 1
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (nf[mid] <= e) lo = mid;
-                            else hi = mid;
+                    if (p.want_sys) {
+                        const int f0 = nf[cc], nn = nf[cc + 1] - f0;
+                        for (int q = lane; q < nn; q += 32) {
+                            p.ff_row_idx[off_f + f0 + q] = f_row[q * TC + cc];
+                            p.ff_values[off_f + f0 + q] = f_val[q * TC + cc];
                         }
-                        const int q = e - nf[lo];
-                        p.ff_row_idx[off_f + e] = f_row[q * TC + lo];
-                        p.ff_values[off_f + e] = f_val[q * TC + lo];
                     }
+                }
                 if (mine && u == 0) p.col_ptr[c + 1] = (int32_t)(off_a + na[col + 1]);
             }
         }
@@ -533,6 +539,7 @@ int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax) {
     if (dim == 2) {
         if (shape == "32x64") return launch_shape<2, 32, 64>(ctx, p, kmax);
         if (shape == "32x128") return launch_shape<2, 32, 128>(ctx, p, kmax);
+        if (shape == "128x128") return launch_shape<2, 128, 128>(ctx, p, kmax);
         return launch_shape<2, 64, 128>(ctx, p, kmax);
     }
     if (shape == "16x64") return launch_shape<3, 16, 64>(ctx, p, kmax);
