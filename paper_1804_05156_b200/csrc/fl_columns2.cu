@@ -79,7 +79,18 @@ struct Layout {
     static constexpr size_t PTR_OFF = TF_OFF + sizeof(int32_t) * T::HSU * TC;   // int32 [TC+1]
     static constexpr size_t NA_OFF = PTR_OFF + sizeof(int32_t) * (TC + 1);      // int32 [TC+1]
     static constexpr size_t NF_OFF = NA_OFF + sizeof(int32_t) * (TC + 1);       // int32 [TC+1]
-    static constexpr size_t MISC_OFF = (NF_OFF + sizeof(int32_t) * (TC + 1) + 15) & ~size_t(15);
+    // parallel fold (LIFT == false): per-item slot ids and ranks, per (pass, slot)
+    // counts and offsets, per-column item lists, per-slot results
+    static constexpr size_t SL_OFF = NF_OFF + sizeof(int32_t) * (TC + 1);       // u8 [KMAX][NV*TC]
+    static constexpr size_t RK_OFF = SL_OFF + (size_t)KMAX * NV * TC;           // u8 [KMAX][NV*TC]
+    static constexpr size_t CN_OFF = RK_OFF + (size_t)KMAX * NV * TC;           // u8 [NV][HSU][TC]
+    static constexpr size_t PO_OFF = CN_OFF + (size_t)NV * T::HSU * TC;         // u8 [NV][HSU][TC]
+    static constexpr size_t LS_OFF = PO_OFF + (size_t)NV * T::HSU * TC;         // u8 [KMAX*NV][TC]
+    static constexpr size_t TK_OFF = LS_OFF + (size_t)KMAX * NV * TC;           // u8 [HSU][TC] rank
+    static constexpr size_t TN_OFF = TK_OFF + (size_t)T::HSU * TC;              // u8 [HSU][TC] count
+    static constexpr size_t DG_OFF = (TN_OFF + (size_t)T::HSU * TC + 7) & ~size_t(7);  // double [TC]
+    static constexpr size_t NS_OFF = DG_OFF + sizeof(double) * TC;              // int32 [TC] slots
+    static constexpr size_t MISC_OFF = (NS_OFF + sizeof(int32_t) * TC + 15) & ~size_t(15);
     static constexpr size_t BYTES = MISC_OFF + 64;
 };
 
@@ -224,82 +235,86 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         __syncthreads();
 
         FL_MARK(1)
-        // ---- phase 3: folds, P threads per column
+        // ---- phase 3: folds
         const bool mine = col < ncols;
         const int32_t c = c0 + col;
         const int m = mine ? ptr[col + 1] - ptr[col] : 0;
         double b = 0.0, y = 0.0;
         int nown = 0;
-        if (mine && p.want_a) {
-            const int32_t* __restrict__ Rc = R + col;
-            const double* __restrict__ Sc = S + col;
-            int32_t* __restrict__ trow = tab_row + col;
-            double* __restrict__ tacc = tab_acc + col;
+        if constexpr (LIFT) {
+            // general path (Dirichlet lift): one thread per column, hashed slots
+            if (mine && p.want_a) {
+                const int32_t* __restrict__ Rc = R + col;
+                const double* __restrict__ Sc = S + col;
+                int32_t* __restrict__ trow = tab_row + col;
+                double* __restrict__ tacc = tab_acc + col;
 #pragma unroll
-            for (int h = 0; h < T::HSU; ++h) trow[h * TC] = -1;
-            bool over = false;
-            for (int i = 0; i < NV; ++i) {
-                // software pipeline: the next item's row/value are loaded before
-                // the current accumulator update
-                int32_t r_nx = m > 0 ? Rc[i * TC] : 0;
-                double s_nx = m > 0 ? Sc[i * TC] : 0.0;
-                for (int k = 0; k < m; ++k) {
-                    const int32_t r = r_nx;
-                    const double sv = s_nx;
-                    if (k + 1 < m) {
-                        r_nx = Rc[(k + 1) * LY::SROW + i * TC];
-                        s_nx = Sc[(k + 1) * LY::SROW + i * TC];
-                    }
-                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
-                    int slot = -1;
-                    while (true) {
-                        const int32_t kk = trow[h * TC];
-                        if (kk == r) {
-                            slot = (int)h;
-                            break;
+                for (int h = 0; h < T::HSU; ++h) trow[h * TC] = -1;
+                bool over = false;
+                for (int i = 0; i < NV; ++i) {
+                    for (int k = 0; k < m; ++k) {
+                        const int32_t r = Rc[k * LY::SROW + i * TC];
+                        const double sv = Sc[k * LY::SROW + i * TC];
+                        uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
+                        int slot = -1;
+                        while (true) {
+                            const int32_t kk = trow[h * TC];
+                            if (kk == r) {
+                                slot = (int)h;
+                                break;
+                            }
+                            if (kk == -1) {
+                                if (nown >= T::MAXU) break;
+                                trow[h * TC] = r;
+                                tacc[h * TC] = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                                tab_tacc[h * TC + col] = -0.0;
+                                ++nown;
+                                slot = (int)h;
+                                break;
+                            }
+                            h = (h + 1) & (T::HSU - 1);
                         }
-                        if (kk == -1) {
-                            if (nown >= T::MAXU) break;
-                            trow[h * TC] = r;
-                            tacc[h * TC] = -0.0;  // -0.0 + x == x: the fold starts at its first value
-                            if (LIFT) tab_tacc[h * TC + col] = -0.0;
-                            ++nown;
-                            slot = (int)h;
-                            break;
+                        if (slot < 0) {
+                            over = true;
+                            continue;
                         }
-                        h = (h + 1) & (T::HSU - 1);
+                        tacc[slot * TC] = tacc[slot * TC] + sv;
                     }
-                    if (slot < 0) {
-                        over = true;
-                        continue;
-                    }
-                    tacc[slot * TC] = tacc[slot * TC] + sv;
                 }
-            }
-            if (over) misc[3] = 1;
-            if (LIFT && !over) {
-                // entry (c, r) in its own order (i_c*(d+1)+j_r, t): j-buckets of the
-                // ranked incidences (j = local index of c) outer, then i, then t
-                int k0 = 0;
-                while (k0 < m) {
-                    const uint32_t jb = KS[k0 * LY::LROW + col] >> 30;
-                    int k1 = k0;
-                    while (k1 < m && (KS[k1 * LY::LROW + col] >> 30) == jb) ++k1;
-                    for (int i = 0; i < NV; ++i)
-                        for (int k = k0; k < k1; ++k) {
-                            const int32_t r = R[k * LY::SROW + i * TC + col];
-                            uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
-                            while (tab_row[h * TC + col] != r) h = (h + 1) & (T::HSU - 1);
-                            double& a = tab_tacc[h * TC + col];
-                            a = a + S[k * LY::SROW + i * TC + col];
-                        }
-                    k0 = k1;
+                if (over) misc[3] = 1;
+                if (!over) {
+                    // entry (c, r) in its own order (i_c*(d+1)+j_r, t): j-buckets of the
+                    // ranked incidences (j = local index of c) outer, then i, then t
+                    int k0 = 0;
+                    while (k0 < m) {
+                        const uint32_t jb = KS[k0 * LY::LROW + col] >> 30;
+                        int k1 = k0;
+                        while (k1 < m && (KS[k1 * LY::LROW + col] >> 30) == jb) ++k1;
+                        for (int i = 0; i < NV; ++i)
+                            for (int k = k0; k < k1; ++k) {
+                                const int32_t r = R[k * LY::SROW + i * TC + col];
+                                uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
+                                while (tab_row[h * TC + col] != r) h = (h + 1) & (T::HSU - 1);
+                                double& a = tab_tacc[h * TC + col];
+                                a = a + S[k * LY::SROW + i * TC + col];
+                            }
+                        k0 = k1;
+                    }
                 }
             }
         }
         if (mine && u == 0) {
-            if (p.want_b)
-                for (int k = 0; k < m; ++k) b = b + Lb[k * LY::LROW + col];
+            // b = 0.0 + load shares in (j, t) order; the diagonal entry (c, c) is the
+            // fold of s_{j_k j_k} in the same (j, t) order (its items all have i = j)
+            double dg = -0.0;
+            for (int k = 0; k < m; ++k) {
+                if (p.want_b) b = b + Lb[k * LY::LROW + col];
+                if (!LIFT && p.want_a) {
+                    const int jk = (int)(KS[k * LY::LROW + col] >> 30);
+                    dg = dg + S[k * LY::SROW + jk * TC + col];
+                }
+            }
+            if (!LIFT && p.want_a) reinterpret_cast<double*>(smem + LY::DG_OFF)[col] = dg;
             // Neumann data (system.hpp:123-172) at nodes on flag-2 faces: face-major
             // (lf, t) order, accumulated from 0.0, then b += add
             if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE && p.is_neu[c]) {
@@ -330,48 +345,44 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                 b = b + add;
             }
         }
-        __syncthreads();  // folds done: the phase-2 buffers become the output lists
-        // free ranks of every slot row, gathered by all threads at once (the
-        // zero-drop loop below would otherwise wait on one gather per entry)
-        if (p.want_sys && p.want_a)
-            for (int e = tid; e < T::HSU * TC; e += T::THREADS) {
-                const int32_t r = tab_row[e];
-                if (r >= 0 && (e % TC) < ncols) tab_fidx[e] = __ldg(p.fidx + r);
-            }
-        __syncthreads();
-        FL_MARK(2)
-
-        // ---- phase 4a: slots -> rows in ascending order, drop exact zeros
-        if (p.want_a) {
-            if (mine && nown <= T::MAXS) {
-                // extract the slots with an insertion sort by row
-                int n = 0;
-                for (int h = 0; h < T::HSU; ++h) {
-                    const int32_t r = tab_row[h * TC + col];
-                    if (r < 0) continue;
-                    const double v = tab_acc[h * TC + col];
-                    const double tv = LIFT ? tab_tacc[h * TC + col] : 0.0;
-                    const int32_t fx = p.want_sys ? tab_fidx[h * TC + col] : -1;
-                    int q = n++;
-                    while (q > 0) {
-                        const int32_t rp = o_row[(q - 1) * TC + col];
-                        if (rp < r) break;
-                        o_row[q * TC + col] = rp;
-                        o_val[q * TC + col] = o_val[(q - 1) * TC + col];
-                        f_row[q * TC + col] = f_row[(q - 1) * TC + col];
-                        if (LIFT) o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
-                        --q;
-                    }
-                    o_row[q * TC + col] = r;
-                    o_val[q * TC + col] = v;
-                    f_row[q * TC + col] = fx;  // free rank of the row (-1: Dirichlet)
-                    if (LIFT) o_tv[q * TC + col] = tv;
+        if constexpr (LIFT) {
+            __syncthreads();  // folds done: the phase-2 buffers become the output lists
+            if (p.want_sys && p.want_a)
+                for (int e = tid; e < T::HSU * TC; e += T::THREADS) {
+                    const int32_t r = tab_row[e];
+                    if (r >= 0 && (e % TC) < ncols) tab_fidx[e] = __ldg(p.fidx + r);
                 }
-            }
-            if (mine) {
-                const int n = nown <= T::MAXS ? nown : 0;
-                // Dirichlet lift: (A u0)[c] = sum over stored A(c, r), ascending r
-                if (LIFT)
+            __syncthreads();
+            FL_MARK(2)
+            if (p.want_a) {
+                if (mine && nown <= T::MAXS) {
+                    // extract the slots with an insertion sort by row
+                    int n = 0;
+                    for (int h = 0; h < T::HSU; ++h) {
+                        const int32_t r = tab_row[h * TC + col];
+                        if (r < 0) continue;
+                        const double v = tab_acc[h * TC + col];
+                        const double tv = tab_tacc[h * TC + col];
+                        const int32_t fx = p.want_sys ? tab_fidx[h * TC + col] : -1;
+                        int q = n++;
+                        while (q > 0) {
+                            const int32_t rp = o_row[(q - 1) * TC + col];
+                            if (rp < r) break;
+                            o_row[q * TC + col] = rp;
+                            o_val[q * TC + col] = o_val[(q - 1) * TC + col];
+                            f_row[q * TC + col] = f_row[(q - 1) * TC + col];
+                            o_tv[q * TC + col] = o_tv[(q - 1) * TC + col];
+                            --q;
+                        }
+                        o_row[q * TC + col] = r;
+                        o_val[q * TC + col] = v;
+                        f_row[q * TC + col] = fx;  // free rank of the row (-1: Dirichlet)
+                        o_tv[q * TC + col] = tv;
+                    }
+                }
+                if (mine) {
+                    const int n = nown <= T::MAXS ? nown : 0;
+                    // Dirichlet lift: (A u0)[c] = sum over stored A(c, r), ascending r
                     for (int q = 0; q < n; ++q) {
                         const int32_t r = o_row[q * TC + col];
                         const double a_cr = o_tv[q * TC + col];
@@ -380,26 +391,206 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                             if (uu != 0.0) y = y + a_cr * uu;
                         }
                     }
-                const bool col_free = p.want_sys && p.fidx[c] >= 0;
-                int ka = 0, kf = 0;
-                for (int q = 0; q < n; ++q) {
-                    const int32_t r = o_row[q * TC + col];
-                    const double v = o_val[q * TC + col];
-                    const int32_t fr = f_row[q * TC + col];
-                    if (v == 0.0) continue;  // sparse.hpp:105
-                    o_row[ka * TC + col] = r;
-                    o_val[ka * TC + col] = v;
-                    ++ka;
-                    if (col_free) {
-                        if (fr >= 0) {
+                    const bool col_free = p.want_sys && p.fidx[c] >= 0;
+                    int ka = 0, kf = 0;
+                    for (int q = 0; q < n; ++q) {
+                        const int32_t r = o_row[q * TC + col];
+                        const double v = o_val[q * TC + col];
+                        const int32_t fr = f_row[q * TC + col];
+                        if (v == 0.0) continue;  // sparse.hpp:105
+                        o_row[ka * TC + col] = r;
+                        o_val[ka * TC + col] = v;
+                        ++ka;
+                        if (col_free && fr >= 0) {
                             f_row[kf * TC + col] = fr;
                             f_val[kf * TC + col] = v;
                             ++kf;
                         }
                     }
+                    na[col] = ka;
+                    nf[col] = kf;
                 }
-                na[col] = ka;
-                nf[col] = kf;
+            }
+        } else if (p.want_a) {
+            // parallel path: every thread works on every step
+            uint8_t* SLb = smem + LY::SL_OFF;  // slot of item (k, i, col)
+            uint8_t* RKb = smem + LY::RK_OFF;  // rank of the item inside its (pass, slot)
+            uint8_t* CNb = smem + LY::CN_OFF;  // items per (pass, slot)
+            uint8_t* POb = smem + LY::PO_OFF;  // list offset of (pass, slot)
+            uint8_t* LSb = smem + LY::LS_OFF;  // per-column item list, codes k*NV + i
+            uint8_t* TKb = smem + LY::TK_OFF;  // sorted position of a slot's row
+            uint8_t* TNb = smem + LY::TN_OFF;  // items of a slot
+            const double* DG = reinterpret_cast<const double*>(smem + LY::DG_OFF);
+            int32_t* NS = reinterpret_cast<int32_t*>(smem + LY::NS_OFF);
+            constexpr int IS = NV * TC;  // item-row stride of SL/RK
+            constexpr int HT = T::HSU * TC;
+            constexpr int G = T::HSU;     // lanes per column group (16 or 32)
+            constexpr int GPW = 32 / G;   // column groups per warp
+            constexpr int NW = T::THREADS / 32;
+            const int lane = tid & 31, wid = tid >> 5, gl = lane % G, gi = lane / G;
+            for (int e = tid; e < HT; e += T::THREADS) tab_row[e] = -1;
+            __syncthreads();
+            // F1: slot of every item -- shared hash insert, CAS only for new rows
+            bool over = false;
+            for (int pos = tid; pos < KMAX * TC; pos += T::THREADS) {
+                const int k = pos / TC, cc = pos - k * TC;
+                if (cc >= ncols || k >= ptr[cc + 1] - ptr[cc]) continue;
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const int32_t r = R[k * LY::SROW + i * TC + cc];
+                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - LOGH);
+                    int probes = 0;
+                    while (true) {
+                        const int32_t v = tab_row[h * TC + cc];
+                        if (v == r) break;
+                        if (v == -1) {
+                            const int32_t old = atomicCAS(&tab_row[h * TC + cc], -1, r);
+                            if (old == -1 || old == r) break;
+                        }
+                        h = (h + 1) & (T::HSU - 1);
+                        if (++probes > T::HSU) {
+                            over = true;
+                            break;
+                        }
+                    }
+                    SLb[k * IS + i * TC + cc] = (uint8_t)h;
+                }
+            }
+            if (over) misc[3] = 1;
+            __syncthreads();
+            // F2: per (pass, column): stable rank of each item among its slot's items
+            for (int task = tid; task < IS; task += T::THREADS) {
+                const int i = task / TC, cc = task - i * TC;
+                if (cc >= ncols) continue;
+                uint8_t* cn = CNb + i * HT + cc;
+#pragma unroll
+                for (int h = 0; h < T::HSU; ++h) cn[h * TC] = 0;
+                const int m2 = ptr[cc + 1] - ptr[cc];
+                for (int k = 0; k < m2; ++k) {
+                    const int s = SLb[k * IS + i * TC + cc];
+                    const uint8_t x = cn[s * TC];
+                    RKb[k * IS + i * TC + cc] = x;
+                    cn[s * TC] = x + 1;
+                }
+            }
+            __syncthreads();
+            // F3: per column (G lanes = G table entries): item counts, list offsets,
+            // sorted position of each row
+            for (int cc = wid * GPW + gi; cc < TC; cc += NW * GPW) {
+                const bool act = cc < ncols;
+                const int32_t r = act ? tab_row[gl * TC + cc] : -1;
+                const bool valid = r >= 0;
+                int ni[NV], nh = 0;
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    ni[i] = valid ? CNb[i * HT + gl * TC + cc] : 0;
+                    nh += ni[i];
+                }
+                int incl = nh;
+#pragma unroll
+                for (int o = 1; o < G; o <<= 1) {
+                    const int yv = __shfl_up_sync(0xffffffffu, incl, o, G);
+                    if (gl >= o) incl += yv;
+                }
+                int run = incl - nh;
+                int rank = 0;
+#pragma unroll 8
+                for (int q = 0; q < G; ++q) {
+                    const int32_t rq = __shfl_sync(0xffffffffu, r, q, G);
+                    rank += (rq >= 0) & (rq < r);
+                }
+                const unsigned bv = __ballot_sync(0xffffffffu, valid);
+                const int nvalid = __popc(G == 32 ? bv : (bv >> (gi * G)) & ((1u << G) - 1));
+                if (valid) {
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) {
+                        POb[i * HT + gl * TC + cc] = (uint8_t)run;
+                        run += ni[i];
+                    }
+                    TKb[gl * TC + cc] = (uint8_t)rank;
+                    TNb[gl * TC + cc] = (uint8_t)nh;
+                }
+                if (gl == 0 && act) {
+                    NS[cc] = nvalid;
+                    if (nvalid > T::MAXS) misc[3] = 1;
+                }
+            }
+            __syncthreads();
+            // F4: item codes into each column's list, ordered by (slot, pass, k)
+            for (int task = tid; task < IS; task += T::THREADS) {
+                const int i = task / TC, cc = task - i * TC;
+                if (cc >= ncols) continue;
+                const int m2 = ptr[cc + 1] - ptr[cc];
+                for (int k = 0; k < m2; ++k) {
+                    const int s = SLb[k * IS + i * TC + cc];
+                    const int pos = POb[i * HT + s * TC + cc] + RKb[k * IS + i * TC + cc];
+                    LSb[pos * TC + cc] = (uint8_t)(k * NV + i);
+                }
+            }
+            __syncthreads();
+            // F5: each off-diagonal entry = sequential fold of its list, i.e. in the
+            // reference order (i*(d+1)+j, t); the diagonal comes from the column thread
+            for (int e = tid; e < HT; e += T::THREADS) {
+                const int h = e / TC, cc = e - h * TC;
+                const int32_t r = tab_row[e];
+                if (r < 0 || cc >= ncols) continue;
+                double acc;
+                if (r == c0 + cc) {
+                    acc = DG[cc];
+                } else {
+                    const int base = POb[h * TC + cc];
+                    const int n = TNb[e];
+                    acc = -0.0;
+                    for (int q = 0; q < n; ++q) {
+                        const int code = LSb[(base + q) * TC + cc];
+                        const int kk = code / NV, ii = code - kk * NV;
+                        acc = acc + S[kk * LY::SROW + ii * TC + cc];
+                    }
+                }
+                tab_acc[e] = acc;
+                if (p.want_sys) tab_fidx[e] = __ldg(p.fidx + r);
+            }
+            __syncthreads();  // S is dead: the output lists may overwrite it
+            FL_MARK(2)
+            // F6: rows in ascending order, exact zeros dropped, A(free, free) rows
+            for (int cc = wid * GPW + gi; cc < TC; cc += NW * GPW) {
+                const bool act = cc < ncols;
+                const int32_t r = act ? tab_row[gl * TC + cc] : -1;
+                if (r >= 0) {
+                    const int q = TKb[gl * TC + cc];
+                    o_row[q * TC + cc] = r;
+                    o_val[q * TC + cc] = tab_acc[gl * TC + cc];
+                    f_row[q * TC + cc] = p.want_sys ? tab_fidx[gl * TC + cc] : -1;
+                }
+                __syncwarp();
+                const int n = act ? NS[cc] : 0;
+                const bool in = gl < n && n <= T::MAXS;
+                const int32_t rr = in ? o_row[gl * TC + cc] : 0;
+                const double vv = in ? o_val[gl * TC + cc] : 0.0;
+                const int32_t ff = in ? f_row[gl * TC + cc] : -1;
+                const bool col_free = act && p.want_sys && __ldg(p.fidx + c0 + cc) >= 0;
+                const bool keep = in && vv != 0.0;  // sparse.hpp:105
+                const bool keep_f = keep && col_free && ff >= 0;
+                const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << (gi * G));
+                const unsigned ba = __ballot_sync(0xffffffffu, keep) & gmask;
+                const unsigned bf = __ballot_sync(0xffffffffu, keep_f) & gmask;
+                const unsigned lower = (1u << lane) - 1;
+                __syncwarp();
+                if (keep) {
+                    const int pa = __popc(ba & lower);
+                    o_row[pa * TC + cc] = rr;
+                    o_val[pa * TC + cc] = vv;
+                }
+                if (keep_f) {
+                    const int pf = __popc(bf & lower);
+                    f_row[pf * TC + cc] = ff;
+                    f_val[pf * TC + cc] = vv;
+                }
+                if (gl == 0 && act) {
+                    na[cc] = __popc(ba);
+                    nf[cc] = __popc(bf);
+                }
+                __syncwarp();
             }
         }
         for (int q = tid; q < TC; q += T::THREADS)
