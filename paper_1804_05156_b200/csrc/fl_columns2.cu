@@ -729,10 +729,13 @@ int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax) {
     const std::string shape = env ? env : "";
     if (dim == 2) {
         if (shape == "32x64") return launch_shape<2, 32, 64>(ctx, p, kmax);
+        if (shape == "16x64") return launch_shape<2, 16, 64>(ctx, p, kmax);
         if (shape == "32x128") return launch_shape<2, 32, 128>(ctx, p, kmax);
         if (shape == "128x128") return launch_shape<2, 128, 128>(ctx, p, kmax);
         return launch_shape<2, 64, 128>(ctx, p, kmax);
     }
+    if (shape == "8x64") return launch_shape<3, 8, 64>(ctx, p, kmax);
+    if (shape == "8x32") return launch_shape<3, 8, 32>(ctx, p, kmax);
     if (shape == "16x64") return launch_shape<3, 16, 64>(ctx, p, kmax);
     if (shape == "16x128") return launch_shape<3, 16, 128>(ctx, p, kmax);
     if (shape == "32x64") return launch_shape<3, 32, 64>(ctx, p, kmax);
