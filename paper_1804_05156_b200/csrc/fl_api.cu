@@ -490,7 +490,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
             } else {
-                FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc));
+                FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
             }
         }
     }

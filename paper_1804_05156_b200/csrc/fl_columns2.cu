@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         if (tid < ncols) too_big = ptr[tid + 1] - ptr[tid] > KMAX;
         if (__syncthreads_or(too_big)) {
             if (tid == 0) atomicOr(p.err, DERR_V2_OVERFLOW);
-            if (tid < 32) warp_lookback(p.tile_status, tile, 0);  // keep the chain alive
+            if (tid == 0) p.tile_tot[tile] = p.tile_tot[p.n_tiles + 1 + tile] = 0;
             __syncthreads();
             continue;
         }
@@ -598,7 +598,8 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
         __syncthreads();
 
         FL_MARK(3)
-        // ---- phase 4b: tile prefix, look-back, coalesced writes
+        // ---- phase 4b: in-tile prefix, staged writes (offsets resolved later by
+        //      a scan over tile totals and k_stage_copy: no waiting on other tiles)
         if (tid < 32) {
             constexpr int PER = (TC + 31) / 32;  // columns per lane
             int va[PER], vf[PER], sa = 0, sf = 0;
@@ -637,41 +638,35 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             if (tid == 0) {
                 na[TC] = ta;
                 nf[TC] = tf;
-            }
-            const uint64_t ex =
-                warp_lookback(p.tile_status, tile, ((uint64_t)tf << 31) | (uint64_t)ta);
-            if (tid == 0) {
-                misc[1] = (int64_t)(ex & 0x7FFFFFFFull);
-                misc[2] = (int64_t)(ex >> 31);
+                p.tile_tot[tile] = ta;
+                p.tile_tot[p.n_tiles + 1 + tile] = tf;
                 if (misc[3]) atomicOr(p.err, DERR_V2_OVERFLOW);
             }
         }
         __syncthreads();
         FL_MARK(4)
-        const int64_t off_a = misc[1], off_f = misc[2];
-        const int ta = na[TC], tf = nf[TC];
         if (p.want_a) {
-            if (off_a + ta > p.cap_a || (p.want_sys && off_f + tf > p.cap_ff)) {
-                if (tid == 0) atomicOr(p.err, DERR_CAPACITY);
-            } else {
-                // a warp per column: each column's entries are one contiguous run
-                constexpr int NW = T::THREADS / 32;
-                const int lane = tid & 31, wid = tid >> 5;
-                for (int cc = wid; cc < ncols; cc += NW) {
-                    const int b0 = na[cc], n = na[cc + 1] - b0;
-                    for (int q = lane; q < n; q += 32) {
-                        p.row_idx[off_a + b0 + q] = o_row[q * TC + cc];
-                        p.values[off_a + b0 + q] = o_val[q * TC + cc];
-                    }
-                    if (p.want_sys) {
-                        const int f0 = nf[cc], nn = nf[cc + 1] - f0;
-                        for (int q = lane; q < nn; q += 32) {
-                            p.ff_row_idx[off_f + f0 + q] = f_row[q * TC + cc];
-                            p.ff_values[off_f + f0 + q] = f_val[q * TC + cc];
-                        }
+            const int64_t sbase = tile * p.tile_cap;
+            // a warp per column: each column's entries are one contiguous run
+            constexpr int NW = T::THREADS / 32;
+            const int lane = tid & 31, wid = tid >> 5;
+            for (int cc = wid; cc < ncols; cc += NW) {
+                const int b0 = na[cc], n = na[cc + 1] - b0;
+                for (int q = lane; q < n; q += 32) {
+                    p.st_a_row[sbase + b0 + q] = o_row[q * TC + cc];
+                    p.st_a_val[sbase + b0 + q] = o_val[q * TC + cc];
+                }
+                if (p.want_sys) {
+                    const int f0 = nf[cc], nn = nf[cc + 1] - f0;
+                    for (int q = lane; q < nn; q += 32) {
+                        p.st_f_row[sbase + f0 + q] = f_row[q * TC + cc];
+                        p.st_f_val[sbase + f0 + q] = f_val[q * TC + cc];
                     }
                 }
-                if (mine && u == 0) p.col_ptr[c + 1] = (int32_t)(off_a + na[col + 1]);
+            }
+            if (mine && u == 0) {
+                p.colcnt_a[c] = na[col + 1];
+                if (p.want_sys) p.colcnt_f[c] = nf[col + 1];
             }
         }
         if (mine && u == 0) {
@@ -682,10 +677,7 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                 p.u0[c] = u0;
                 p.b_mod[c] = bmod;
                 const int32_t fc = p.fidx[c];
-                if (fc >= 0) {
-                    p.b_f[fc] = bmod;
-                    if (p.want_a) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + nf[col + 1]);
-                }
+                if (fc >= 0) p.b_f[fc] = bmod;
             }
         }
         __syncthreads();
@@ -693,53 +685,132 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
     }
 }
 
+// Places the staged tiles: tile t's A entries go to [tile_off_a[t], +tot), and
+// col_ptr[c+1] = tile_off + the in-tile inclusive count (same for A(free,free),
+// whose columns are the free columns in ascending order).
+__global__ void k_stage_copy(ColParams p, int tc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int32_t* off_a = p.tile_off;
+    const int32_t* off_f = p.tile_off + p.n_tiles + 1;
+    const int32_t* tot_a = p.tile_tot;
+    const int32_t* tot_f = p.tile_tot + p.n_tiles + 1;
+    for (int64_t t = warp; t < p.n_tiles; t += nwarps) {
+        const int64_t sbase = t * p.tile_cap;
+        const int32_t oa = off_a[t], na = tot_a[t];
+        if ((int64_t)oa + na > p.cap_a) {
+            if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
+            continue;
+        }
+        for (int q = lane; q < na; q += 32) {
+            p.row_idx[oa + q] = p.st_a_row[sbase + q];
+            p.values[oa + q] = p.st_a_val[sbase + q];
+        }
+        const int32_t c0 = (int32_t)(t * tc);
+        for (int q = lane; q < tc && c0 + q < p.n_nodes; q += 32)
+            p.col_ptr[c0 + q + 1] = oa + p.colcnt_a[c0 + q];
+        if (p.want_sys) {
+            const int32_t of = off_f[t], nf = tot_f[t];
+            for (int q = lane; q < nf; q += 32) {
+                p.ff_row_idx[of + q] = p.st_f_row[sbase + q];
+                p.ff_values[of + q] = p.st_f_val[sbase + q];
+            }
+            for (int q = lane; q < tc && c0 + q < p.n_nodes; q += 32) {
+                const int32_t fc = p.fidx[c0 + q];
+                if (fc >= 0) p.ff_col_ptr[fc + 1] = of + p.colcnt_f[c0 + q];
+            }
+        }
+    }
+}
+
 
 template <int D, int TCX, int THR, int KMAX, bool LIFT>
-static int launch_variant(fl_ctx* ctx, ColParams& p) {
+static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
     using T = Tile<D, TCX, THR>;
     using LY = Layout<T, D, KMAX, LIFT>;
     const size_t smem = LY::BYTES;
     auto kern = k_columns2<D, TCX, THR, KMAX, LIFT>;
+    const cudaStream_t s = ctx->stream;
+    p.n_tiles = (p.n_nodes + TCX - 1) / TCX;
+    p.tile_cap = (int64_t)TCX * T::MAXS;
+    // staging for the compacted per-tile entries and the tile/column counts
+    const size_t nst = (size_t)p.n_tiles * (size_t)p.tile_cap;
+    FL_TRY(res->stage[0].ensure(sizeof(int32_t) * nst));
+    FL_TRY(res->stage[1].ensure(sizeof(double) * nst));
+    if (p.want_sys) {
+        FL_TRY(res->stage[2].ensure(sizeof(int32_t) * nst));
+        FL_TRY(res->stage[3].ensure(sizeof(double) * nst));
+    }
+    FL_TRY(res->tile_tot.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_tiles + 1)));
+    FL_TRY(res->tile_off.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_tiles + 1)));
+    FL_TRY(res->colcnt.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_nodes + 1)));
+    p.st_a_row = res->stage[0].as<int32_t>();
+    p.st_a_val = res->stage[1].as<double>();
+    p.st_f_row = res->stage[2].as<int32_t>();
+    p.st_f_val = res->stage[3].as<double>();
+    p.tile_tot = res->tile_tot.as<int32_t>();
+    p.tile_off = res->tile_off.as<int32_t>();
+    p.colcnt_a = res->colcnt.as<int32_t>();
+    p.colcnt_f = res->colcnt.as<int32_t>() + p.n_nodes + 1;
     FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THR, smem));
-    p.n_tiles = (p.n_nodes + TCX - 1) / TCX;
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    kern<<<(int)grid, THR, smem, ctx->stream>>>(p);
+    kern<<<(int)grid, THR, smem, s>>>(p);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    if (!p.want_a) return FL_OK;
+    // tile offsets (exclusive scans of the tile totals) and the placement copy
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(p.n_tiles)));
+    const int32_t* ta = p.tile_tot;
+    FL_CUDA(launch_scan<int32_t>(
+        p.n_tiles, [ta] __device__(int64_t i) { return (int64_t)ta[i]; }, p.tile_off,
+        ctx->scan_ws.p, s));
+    count_launch(ctx);
+    if (p.want_sys) {
+        const int32_t* tf = p.tile_tot + p.n_tiles + 1;
+        FL_CUDA(launch_scan<int32_t>(
+            p.n_tiles, [tf] __device__(int64_t i) { return (int64_t)tf[i]; },
+            p.tile_off + p.n_tiles + 1, ctx->scan_ws.p, s));
+        count_launch(ctx);
+    }
+    const int64_t warps = std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * 64);
+    k_stage_copy<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(p, TCX);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;
 }
 
 template <int D, int TCX, int THR>
-static int launch_shape(fl_ctx* ctx, ColParams& p, int kmax) {
+static int launch_shape(fl_ctx* ctx, ColParams& p, int kmax, fl_result* res) {
     constexpr int K_SMALL = D == 2 ? 8 : 24, K_LARGE = D == 2 ? 16 : 32;
     if (kmax <= K_SMALL)
-        return p.need_lift ? launch_variant<D, TCX, THR, K_SMALL, true>(ctx, p)
-                           : launch_variant<D, TCX, THR, K_SMALL, false>(ctx, p);
-    return p.need_lift ? launch_variant<D, TCX, THR, K_LARGE, true>(ctx, p)
-                       : launch_variant<D, TCX, THR, K_LARGE, false>(ctx, p);
+        return p.need_lift ? launch_variant<D, TCX, THR, K_SMALL, true>(ctx, p, res)
+                           : launch_variant<D, TCX, THR, K_SMALL, false>(ctx, p, res);
+    return p.need_lift ? launch_variant<D, TCX, THR, K_LARGE, true>(ctx, p, res)
+                       : launch_variant<D, TCX, THR, K_LARGE, false>(ctx, p, res);
 }
 
 // kmax: the plan's largest node valence (incidences per node).  FL_TILE=<TC>x<THREADS>
 // selects an alternative tile shape (tuning experiments).
-int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax) {
+int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res) {
     const char* env = std::getenv("FL_TILE");
     const std::string shape = env ? env : "";
     if (dim == 2) {
-        if (shape == "32x64") return launch_shape<2, 32, 64>(ctx, p, kmax);
-        if (shape == "16x64") return launch_shape<2, 16, 64>(ctx, p, kmax);
-        if (shape == "32x128") return launch_shape<2, 32, 128>(ctx, p, kmax);
-        if (shape == "128x128") return launch_shape<2, 128, 128>(ctx, p, kmax);
-        return launch_shape<2, 64, 128>(ctx, p, kmax);
+        if (shape == "32x64") return launch_shape<2, 32, 64>(ctx, p, kmax, res);
+        if (shape == "16x64") return launch_shape<2, 16, 64>(ctx, p, kmax, res);
+        if (shape == "32x128") return launch_shape<2, 32, 128>(ctx, p, kmax, res);
+        if (shape == "128x128") return launch_shape<2, 128, 128>(ctx, p, kmax, res);
+        return launch_shape<2, 64, 128>(ctx, p, kmax, res);
     }
-    if (shape == "8x64") return launch_shape<3, 8, 64>(ctx, p, kmax);
-    if (shape == "8x32") return launch_shape<3, 8, 32>(ctx, p, kmax);
-    if (shape == "16x64") return launch_shape<3, 16, 64>(ctx, p, kmax);
-    if (shape == "16x128") return launch_shape<3, 16, 128>(ctx, p, kmax);
-    if (shape == "32x64") return launch_shape<3, 32, 64>(ctx, p, kmax);
-    return launch_shape<3, 32, 128>(ctx, p, kmax);
+    if (shape == "8x64") return launch_shape<3, 8, 64>(ctx, p, kmax, res);
+    if (shape == "8x32") return launch_shape<3, 8, 32>(ctx, p, kmax, res);
+    if (shape == "16x64") return launch_shape<3, 16, 64>(ctx, p, kmax, res);
+    if (shape == "16x128") return launch_shape<3, 16, 128>(ctx, p, kmax, res);
+    if (shape == "32x64") return launch_shape<3, 32, 64>(ctx, p, kmax, res);
+    return launch_shape<3, 32, 128>(ctx, p, kmax, res);
 }
 
 }  // namespace fl

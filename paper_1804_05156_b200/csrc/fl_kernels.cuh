@@ -36,6 +36,17 @@ struct ColParams {
     uint32_t* err;
     int64_t cap_a, cap_ff;
     unsigned long long* phase_cycles;  // diagnostics: per-phase SM cycles (nullptr = off)
+    // tiled kernel staging (no in-kernel look-back): tile t writes its compacted
+    // entries at [t * tile_cap, ...) and its totals; k_stage_copy places them
+    int64_t tile_cap;
+    int32_t* st_a_row;
+    double* st_a_val;
+    int32_t* st_f_row;
+    double* st_f_val;
+    int32_t* tile_tot;   // [2][n_tiles + 1]: A totals, then A(free,free) totals
+    int32_t* tile_off;   // [2][n_tiles + 1]: exclusive scans of tile_tot
+    int32_t* colcnt_a;   // [N] in-tile inclusive count after column c
+    int32_t* colcnt_f;   // [N] same for A(free, free) (indexed by column c)
 };
 
 int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);
@@ -48,7 +59,7 @@ int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
                      int32_t* row_map, int32_t* cnt, uint32_t* d_err, int64_t* nnz_out);
 int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
                         double* qi);
-int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax);
+int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
 size_t column_smem_bytes();
 int column_tile_width();
