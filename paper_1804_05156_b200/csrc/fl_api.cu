@@ -485,12 +485,17 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         x->last_mesh = mesh;
         x->last_valid = true;
         if (N > 0) {
+            // v3 (register-centric) by default; v2 (tiled) carries the Dirichlet
+            // lift; v1 (general) is the fallback.  FL_KERNEL=1|2|3 forces one.
             const char* kern = std::getenv("FL_KERNEL");
-            if (kern && kern[0] == '1') {
+            const char k = kern ? kern[0] : '0';
+            if (k == '1') {
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
-            } else {
+            } else if (k == '2' || p.need_lift) {
                 FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
+            } else {
+                FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res));
             }
         }
     }

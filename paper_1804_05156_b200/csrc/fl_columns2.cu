@@ -732,9 +732,23 @@ static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
     const size_t smem = LY::BYTES;
     auto kern = k_columns2<D, TCX, THR, KMAX, LIFT>;
     const cudaStream_t s = ctx->stream;
-    p.n_tiles = (p.n_nodes + TCX - 1) / TCX;
-    p.tile_cap = (int64_t)TCX * T::MAXS;
-    // staging for the compacted per-tile entries and the tile/column counts
+    FL_TRY(prepare_staging(ctx, p, res, TCX, (int64_t)TCX * T::MAXS));
+    FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THR, smem));
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    kern<<<(int)grid, THR, smem, s>>>(p);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return finish_staging(ctx, p, TCX);
+}
+
+// staging buffers for a tiled launch with `tc` columns and `cap` entries per tile
+int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap) {
+    (void)ctx;
+    p.n_tiles = (p.n_nodes + tc - 1) / tc;
+    p.tile_cap = cap;
     const size_t nst = (size_t)p.n_tiles * (size_t)p.tile_cap;
     FL_TRY(res->stage[0].ensure(sizeof(int32_t) * nst));
     FL_TRY(res->stage[1].ensure(sizeof(double) * nst));
@@ -753,16 +767,13 @@ static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
     p.tile_off = res->tile_off.as<int32_t>();
     p.colcnt_a = res->colcnt.as<int32_t>();
     p.colcnt_f = res->colcnt.as<int32_t>() + p.n_nodes + 1;
-    FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THR, smem));
-    const int64_t grid = std::max<int64_t>(
-        1, std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    kern<<<(int)grid, THR, smem, s>>>(p);
-    count_launch(ctx);
-    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// tile offsets (exclusive scans of the tile totals) and the placement copy
+int finish_staging(fl_ctx* ctx, ColParams& p, int tc) {
+    const cudaStream_t s = ctx->stream;
     if (!p.want_a) return FL_OK;
-    // tile offsets (exclusive scans of the tile totals) and the placement copy
     FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(p.n_tiles)));
     const int32_t* ta = p.tile_tot;
     FL_CUDA(launch_scan<int32_t>(
@@ -777,7 +788,7 @@ static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
         count_launch(ctx);
     }
     const int64_t warps = std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * 64);
-    k_stage_copy<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(p, TCX);
+    k_stage_copy<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(p, tc);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;

@@ -1,0 +1,348 @@
+// fl_columns3.cu -- the register-centric column kernel (v3), fast path of fl_assemble.
+//
+// A group of L lanes (L = 8 in 2-D, 32 in 3-D; a warp holds 32/L groups) owns
+// one output column c = one reference CSC column.  No block barriers: every warp
+// is independent, so the SM hides latency with occupancy.
+//   1. lane g < m loads incidence key g of c (j << 30 | t, unsorted from the
+//      plan) and the group bitonic-sorts the keys: lane g then holds the g-th
+//      incidence in (j, t) order -- the order in which the reference's
+//      blockwise triplets reach column c (assembly.hpp:486-498 after the stable
+//      passes sparse.hpp:79-89);
+//   2. each lane computes its element's column j: s_ij (i = 0..d) and the load
+//      share (fl_geometry.cuh, FMA-free, exact division);
+//   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
+//      A(c,c) = fold of s_jj in lane order (its items are exactly those), both
+//      by shuffles;
+//   4. off-diagonal items (i != j): per pass i, lanes with the same row are found
+//      with match_any; the pass's group leader inserts the row in the group's
+//      small smem hash (CAS) and broadcasts the slot; the items are then added
+//      to the slot accumulator in rounds of increasing lane rank, so every slot
+//      sums its items in (i, then lane) order = the reference's (i*(d+1)+j, t);
+//   5. slots ranked by row, exact zeros dropped (sparse.hpp:105), A(free,free)
+//      rows kept, all written to the tile staging (k_stage_copy places them).
+// Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, or
+// more distinct rows than the group table holds.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "fl_geometry.cuh"
+#include "fl_internal.cuh"
+#include "fl_kernels.cuh"
+#include "fl_scan.cuh"
+
+namespace fl {
+
+template <int D, int L>
+struct V3 {
+    static constexpr int NV = D + 1;
+    static constexpr int GPW = 32 / L;                 // column groups per warp
+    static constexpr int HS = D == 2 ? 16 : 32;        // slot table entries per group
+    static constexpr int MAXS = D == 2 ? 12 : 24;      // distinct rows accepted per column
+    static constexpr int WTC = D == 2 ? 32 : 8;        // columns per warp tile
+    static constexpr int ITERS = WTC / GPW;            // group iterations per warp tile
+    static constexpr int WARPS = 4;                    // warps per CTA
+};
+
+template <int D, int L>
+struct V3Smem {  // one per group
+    int32_t row[V3<D, L>::HS];
+    double acc[V3<D, L>::HS];
+    int32_t srow[V3<D, L>::HS];
+    double sval[V3<D, L>::HS];
+};
+
+__device__ __forceinline__ double node_field3(const FieldDesc& g, const double* nodes, int dim,
+                                              int32_t k) {
+    if (g.kind == FL_FIELD_SAMPLES) return __ldg(g.samples + k);
+    if (g.kind == FL_FIELD_CONST) return g.value;
+    const double x = nodes[(size_t)k * dim];
+    const double y = nodes[(size_t)k * dim + 1];
+    const double z = dim == 3 ? nodes[(size_t)k * dim + 2] : 0.0;
+    return eval_point(g, x, y, z);
+}
+
+template <int D, int L>
+__global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) {
+    using C = V3<D, L>;
+    constexpr int NV = D + 1;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ V3Smem<D, L> sm_all[C::WARPS * C::GPW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = lane / L, g = lane % L;  // group in warp, lane in group
+    const unsigned gmask = (L == 32) ? FULL : (((1u << L) - 1) << (gi * L));
+    const unsigned lower = (1u << lane) - 1;
+    V3Smem<D, L>& sm = sm_all[warp * C::GPW + gi];
+    const Recip R3 = recip(3.0);
+    const Recip R6 = recip(6.0);
+
+    while (true) {
+        int64_t tile = 0;
+        if (lane == 0) tile = atomicAdd(p.ticket, 1u);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= p.n_tiles) break;
+        const int64_t sbase = tile * p.tile_cap;
+        int run_a = 0, run_f = 0;  // warp-uniform: entries staged so far in this tile
+        bool bad = false;
+        for (int it = 0; it < C::ITERS; ++it) {
+            const int32_t c = (int32_t)(tile * C::WTC) + it * C::GPW + gi;
+            const bool act = c < p.n_nodes;
+            int32_t p0 = 0, m = 0;
+            if (act) {
+                p0 = __ldg(p.inc_ptr + c);
+                m = __ldg(p.inc_ptr + c + 1) - p0;
+            }
+            if (m > L) {
+                bad = true;
+                m = 0;
+            }
+            // ---- 1. keys, sorted ascending inside the group
+            uint32_t key = (g < m) ? __ldg(p.inc + p0 + g) : 0xFFFFFFFFu;
+#pragma unroll
+            for (int k = 2; k <= L; k <<= 1) {
+#pragma unroll
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    const uint32_t o = __shfl_xor_sync(FULL, key, jj, L);
+                    const bool up = (g & k) == 0;
+                    const bool lo = (g & jj) == 0;
+                    key = (lo == up) ? min(key, o) : max(key, o);
+                }
+            }
+            const bool valid = g < m;
+            const int32_t t = (int32_t)(key & 0x3FFFFFFFu);
+            const int j = valid ? (int)(key >> 30) : 0;
+            // ---- 2. geometry of column j of element t
+            int32_t R[NV];
+            double s[NV];
+            double l = 0.0, sjj = 0.0;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                R[i] = -1;
+                s[i] = 0.0;
+            }
+            if (valid) {
+                if constexpr (D == 3) {
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
+                    R[0] = e.x;
+                    R[1] = e.y;
+                    R[2] = e.z;
+                    R[3] = e.w;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t * NV + i);
+                }
+                ElemCol<D> ec;
+                ec.load(p.nodes, R);
+                double meas;
+                if constexpr (D == 2) meas = ec.stiffness_col(j, s);
+                else meas = ec.stiffness_col(j, s, R6);
+                if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
+                if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
+                    double a;
+                    if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
+                    else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t);
+                    else a = ec.coef_c5(R3);
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) s[i] = s[i] * a;
+                }
+                if (p.want_b) {
+                    if constexpr (D == 2) l = ec.load_col(j, t, p.f, R6);
+                    else l = ec.load_col(j, t, meas, p.f);
+                }
+#pragma unroll
+                for (int i = 0; i < NV; ++i)
+                    if (i == j) sjj = s[i];
+            }
+            // ---- 3. b and the diagonal: sequential folds in lane order
+            double b = 0.0, dg = -0.0;
+            const int mmax = __reduce_max_sync(FULL, (unsigned)m);
+            for (int q = 0; q < mmax; ++q) {
+                const double lq = __shfl_sync(FULL, l, q, L);
+                const double sq = __shfl_sync(FULL, sjj, q, L);
+                if (q < m) {
+                    b = b + lq;
+                    dg = dg + sq;
+                }
+            }
+            // ---- 4. off-diagonal slots and their ordered folds
+            if (p.want_a) {
+                for (int h = g; h < C::HS; h += L) sm.row[h] = -1;
+                __syncwarp();
+                int nslot = 0;
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const bool has = valid && i != j;
+                    const uint64_t mk = has ? (((uint64_t)gi << 32) | (uint32_t)R[i])
+                                            : ((1ull << 63) | (uint64_t)lane);
+                    const unsigned gm = __match_any_sync(FULL, mk);
+                    const int rank = __popc(gm & lower);
+                    int slot = -1;
+                    if (has && rank == 0) {
+                        const int32_t r = R[i];
+                        uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                        for (int probe = 0; probe < C::HS; ++probe) {
+                            const int32_t old = atomicCAS(&sm.row[h], -1, r);
+                            if (old == -1) {
+                                sm.acc[h] = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                                slot = (int)h;
+                                break;
+                            }
+                            if (old == r) {
+                                slot = (int)h;
+                                break;
+                            }
+                            h = (h + 1) & (C::HS - 1);
+                        }
+                        if (slot < 0) bad = true;
+                    }
+                    slot = __shfl_sync(FULL, slot, __ffs(gm) - 1);
+                    __syncwarp();
+                    const int rounds = __reduce_max_sync(FULL, has ? (unsigned)__popc(gm) : 0u);
+                    for (int rr = 0; rr < rounds; ++rr) {
+                        if (has && rank == rr && slot >= 0) sm.acc[slot] = sm.acc[slot] + s[i];
+                        __syncwarp();
+                    }
+                }
+                // ---- 5. rows in ascending order (diagonal included), zero drop
+                if (g == 0 && act && m > 0) {
+                    uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                    for (int probe = 0; probe < C::HS; ++probe) {
+                        if (sm.row[h] == -1) {
+                            sm.row[h] = c;
+                            sm.acc[h] = dg;
+                            break;
+                        }
+                        h = (h + 1) & (C::HS - 1);
+                    }
+                }
+                __syncwarp();
+                for (int h = g; h < C::HS; h += L) {
+                    const int32_t r = sm.row[h];
+                    if (r >= 0) {
+                        int rk = 0;
+#pragma unroll 8
+                        for (int q = 0; q < C::HS; ++q) {
+                            const int32_t rq = sm.row[q];
+                            rk += (rq >= 0) & (rq < r);
+                        }
+                        if (rk < C::MAXS) {
+                            sm.srow[rk] = r;
+                            sm.sval[rk] = sm.acc[h];
+                        }
+                    }
+                }
+                int nv = 0;
+                for (int h = g; h < C::HS; h += L) nv += sm.row[h] >= 0;
+#pragma unroll
+                for (int o = L / 2; o > 0; o >>= 1) nv += __shfl_xor_sync(FULL, nv, o, L);
+                if (nv > C::MAXS) {
+                    bad = true;
+                    nv = 0;
+                }
+                nslot = nv;
+                __syncwarp();
+                const bool col_free = act && p.want_sys && __ldg(p.fidx + c) >= 0;
+                int na = 0, nf = 0;
+                // compaction in chunks of L entries; pass 1: counts per group
+                for (int base = 0; base < C::MAXS; base += L) {
+                    const int q = base + g;
+                    const bool in = q < nslot;
+                    const double v = in ? sm.sval[q] : 0.0;
+                    const int32_t r = in ? sm.srow[q] : 0;
+                    const bool keep = in && v != 0.0;  // sparse.hpp:105
+                    const bool keepf = keep && col_free && __ldg(p.fidx + r) >= 0;
+                    na += __popc(__ballot_sync(FULL, keep) & gmask);
+                    nf += __popc(__ballot_sync(FULL, keepf) & gmask);
+                }
+                // exclusive prefix over the groups of the warp (column order)
+                int pa = na, pf = nf;
+#pragma unroll
+                for (int o = L; o < 32; o <<= 1) {
+                    const int ya = __shfl_up_sync(FULL, pa, o);
+                    const int yf = __shfl_up_sync(FULL, pf, o);
+                    if (lane >= o) {
+                        pa += ya;
+                        pf += yf;
+                    }
+                }
+                const int tot_a = __shfl_sync(FULL, pa, 31), tot_f = __shfl_sync(FULL, pf, 31);
+                int wa = run_a + pa - na, wf = run_f + pf - nf;  // this column's first slot
+                if (act && g == 0) {
+                    p.colcnt_a[c] = wa + na;
+                    if (p.want_sys) p.colcnt_f[c] = wf + nf;
+                }
+                // pass 2: write
+                for (int base = 0; base < C::MAXS; base += L) {
+                    const int q = base + g;
+                    const bool in = q < nslot;
+                    const double v = in ? sm.sval[q] : 0.0;
+                    const int32_t r = in ? sm.srow[q] : 0;
+                    const bool keep = in && v != 0.0;
+                    const int32_t fr = (keep && col_free) ? __ldg(p.fidx + r) : -1;
+                    const bool keepf = fr >= 0;
+                    const unsigned ba = __ballot_sync(FULL, keep) & gmask;
+                    const unsigned bf = __ballot_sync(FULL, keepf) & gmask;
+                    if (keep) {
+                        const int64_t o = sbase + wa + __popc(ba & lower);
+                        p.st_a_row[o] = r;
+                        p.st_a_val[o] = v;
+                    }
+                    if (keepf) {
+                        const int64_t o = sbase + wf + __popc(bf & lower);
+                        p.st_f_row[o] = fr;
+                        p.st_f_val[o] = v;
+                    }
+                    wa += __popc(ba);
+                    wf += __popc(bf);
+                }
+                run_a += tot_a;
+                run_f += tot_f;
+                __syncwarp();
+            }
+            // ---- per-column vectors
+            if (act && g == 0) {
+                if (p.want_b) p.b[c] = b;
+                if (p.want_sys) {
+                    const double u0 = p.is_dir[c] ? node_field3(p.g_dir, p.nodes, D, c) : 0.0;
+                    const double bmod = b - 0.0;  // no lift on this path (g == 0)
+                    p.u0[c] = u0;
+                    p.b_mod[c] = bmod;
+                    const int32_t fc = p.fidx[c];
+                    if (fc >= 0) p.b_f[fc] = bmod;
+                }
+            }
+        }
+        if (lane == 0) {
+            p.tile_tot[tile] = run_a;
+            p.tile_tot[p.n_tiles + 1 + tile] = run_f;
+        }
+        if (__any_sync(FULL, bad) && lane == 0) atomicOr(p.err, DERR_V2_OVERFLOW);
+    }
+}
+
+template <int D, int L>
+static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
+    using C = V3<D, L>;
+    FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
+    int per_sm = 1;
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L>, C::WARPS * 32, 0));
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS,
+                             (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    k_columns3<D, L><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return finish_staging(ctx, p, C::WTC);
+}
+
+// kmax: the plan's largest node valence; need_lift meshes use the tiled kernel
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res) {
+    if (dim == 2) {
+        if (kmax <= 8) return launch3<2, 8>(ctx, p, res);
+        return launch3<2, 16>(ctx, p, res);
+    }
+    return launch3<3, 32>(ctx, p, res);
+}
+
+}  // namespace fl

@@ -60,6 +60,9 @@ int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
 int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
                         double* qi);
 int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
+int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
+int finish_staging(fl_ctx* ctx, ColParams& p, int tc);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
 size_t column_smem_bytes();
 int column_tile_width();
