@@ -492,7 +492,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             if (k == '1') {
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
-            } else if (k == '2' || p.need_lift) {
+            } else if (k == '2' || p.need_lift || (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)) {
                 FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
             } else {
                 FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res));
