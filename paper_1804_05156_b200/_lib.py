@@ -39,6 +39,7 @@ SIGNATURES = {
     "fl_mesh_set_elems": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "fl_mesh_validate": (C.c_int, [_vp, _vp]),
     "fl_mesh_plan": (C.c_int, [_vp, _vp]),
+    "fl_mesh_set_columns": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32]),
     "fl_mesh_destroy": (C.c_int, [_vp]),
     "fl_result_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fl_result_destroy": (C.c_int, [_vp]),
@@ -64,7 +65,7 @@ class Field(C.Structure):
 
 class Sizes(C.Structure):
     _fields_ = [("n", C.c_int32), ("n_dir", C.c_int32), ("n_free", C.c_int32),
-                ("n_dir_faces", C.c_int32), ("n_neu_faces", C.c_int32), ("pad", C.c_int32),
+                ("n_dir_faces", C.c_int32), ("n_neu_faces", C.c_int32), ("n_free_cols", C.c_int32),
                 ("nnz", C.c_int64), ("nnz_ff", C.c_int64)]
 
 

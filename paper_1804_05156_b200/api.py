@@ -183,20 +183,23 @@ class AssemblyResult:
 
     # typed views
     def matrix(self) -> CscMatrix:
+        """A, or this shard's columns of A (rows stay global: m = all nodes)."""
         s = self.sizes()
-        return CscMatrix(s.n, s.n, self.array(_lib.A_COL_PTR, np.int32, s.n + 1),
+        m = getattr(self, "_rows", s.n)
+        return CscMatrix(m, s.n, self.array(_lib.A_COL_PTR, np.int32, s.n + 1),
                          self.array(_lib.A_ROW_IDX, np.int32, s.nnz),
                          self.array(_lib.A_VALUES, np.float64, s.nnz))
 
     def matrix_ff(self) -> CscMatrix:
         s = self.sizes()
-        return CscMatrix(s.n_free, s.n_free, self.array(_lib.AFF_COL_PTR, np.int32, s.n_free + 1),
+        return CscMatrix(s.n_free, s.n_free_cols,
+                         self.array(_lib.AFF_COL_PTR, np.int32, s.n_free_cols + 1),
                          self.array(_lib.AFF_ROW_IDX, np.int32, s.nnz_ff),
                          self.array(_lib.AFF_VALUES, np.float64, s.nnz_ff))
 
     def vector(self, which: int) -> np.ndarray:
         s = self.sizes()
-        n = s.n_free if which == _lib.B_F else s.n
+        n = s.n_free_cols if which == _lib.B_F else s.n
         return self.array(which, np.float64, n)
 
     def partition(self) -> BoundaryPartition:
@@ -214,10 +217,12 @@ class AssemblyResult:
 
 
 def run(mesh: Mesh, what: int, f=None, coef=None, g_dirichlet=None, g_neumann=None,
-        ctx: Optional[Context] = None, result: Optional[AssemblyResult] = None) -> AssemblyResult:
-    """One fl_assemble call (asynchronous; sizes() synchronises)."""
+        ctx: Optional[Context] = None, result: Optional[AssemblyResult] = None,
+        device_mesh=None) -> AssemblyResult:
+    """One fl_assemble call (asynchronous; sizes() synchronises).  ``device_mesh``
+    overrides the mesh's cached device copy (e.g. one restricted to a column range)."""
     ctx = ctx or Context.default()
-    dm = mesh.device(ctx)
+    dm = device_mesh or mesh.device(ctx)
     res = result or AssemblyResult(ctx)
     ff, k1 = _field_struct(f, mesh, "load")
     fc, k2 = _field_struct(coef, mesh, "coef")
@@ -226,6 +231,8 @@ def run(mesh: Mesh, what: int, f=None, coef=None, g_dirichlet=None, g_neumann=No
     _lib.check(_lib.lib().fl_assemble(ctx.handle, dm.handle, C.byref(ff), C.byref(fc), C.byref(fd),
                                       C.byref(fn), what, res.handle), "fl_assemble")
     res._keep = (k1, k2, k3, k4)
+    res._rows = mesh.num_nodes()
+    res._what = what
     return res
 
 

@@ -123,7 +123,7 @@ static int rerun_general(fl_result* res, fl_result_ext* x) {
     FL_CUDA(cudaMemsetAsync(counters + CNT_TICKET, 0, sizeof(uint32_t), ctx->stream));
     FL_CUDA(cudaMemsetAsync(counters + CNT_ERR, 0, sizeof(uint32_t), ctx->stream));
     const int tw = column_tile_width();
-    p.n_tiles = (mesh->n_nodes + tw - 1) / tw;
+    p.n_tiles = (p.n_cols + tw - 1) / tw;
     FL_CUDA(cudaMemsetAsync(res->tile_status.p, 0, sizeof(uint64_t) * ((size_t)p.n_tiles + 1),
                             ctx->stream));
     FL_TRY(launch_columns(ctx, mesh->dim, p));
@@ -226,6 +226,8 @@ FL_API int fl_mesh_create(fl_ctx* ctx, int dim, int32_t n_nodes, int32_t n_elems
     m->dim = dim;
     m->n_nodes = n_nodes;
     m->n_elems = n_elems;
+    m->col_begin = 0;
+    m->col_end = n_nodes;
     const size_t nv = (size_t)dim + 1;
     int rc = copy_in(ctx, m->nodes, nodes, sizeof(double) * (size_t)n_nodes * dim, mem);
     if (!rc) rc = copy_in(ctx, m->elems, elems, sizeof(int32_t) * (size_t)n_elems * nv, mem);
@@ -262,6 +264,16 @@ FL_API int fl_mesh_set_elems(fl_ctx* ctx, fl_mesh* mesh, const int32_t* elems, i
     mesh->planned = false;
     return copy_in(ctx, mesh->elems, elems, sizeof(int32_t) * (size_t)mesh->n_elems * (mesh->dim + 1),
                    mem);
+}
+
+FL_API int fl_mesh_set_columns(fl_ctx* ctx, fl_mesh* mesh, int32_t col_begin, int32_t col_end) {
+    if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (col_begin < 0 || col_end < col_begin || col_end > mesh->n_nodes)
+        return set_error(FL_E_INDEX_OUT_OF_RANGE, "column range outside [0, n_nodes]");
+    if (col_begin != mesh->col_begin || col_end != mesh->col_end) mesh->planned = false;
+    mesh->col_begin = col_begin;
+    mesh->col_end = col_end;
+    return FL_OK;
 }
 
 FL_API int fl_mesh_destroy(fl_mesh* mesh) {
@@ -383,10 +395,12 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     fl_result_ext* x = ext_of(res);
     res->sizes_valid = false;
     res->what = what;
-    res->n = mesh->n_nodes;
-    res->m = mesh->n_nodes;
-    res->dim = mesh->dim;
     const int32_t N = mesh->n_nodes;
+    const int32_t C0 = mesh->col_begin, NC = mesh->col_end - mesh->col_begin;
+    res->n = NC;
+    res->m = N;
+    res->col_begin = C0;
+    res->dim = mesh->dim;
     const int64_t NT = mesh->n_elems;
     const int nv = mesh->dim + 1;
     const bool want_a = what & FL_OUT_STIFFNESS, want_b = what & FL_OUT_LOAD;
@@ -399,18 +413,18 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     FL_TRY(field_desc(ctx, g_neumann, NT * nv, x->stage.g_neu, &p.g_neu, "g_neumann"));
     x->g_missing = want_sys && p.g_dir.kind == FL_FIELD_NONE;
 
-    // outputs
-    const size_t n1 = (size_t)N + 1;
+    // outputs (column-indexed ones hold the owned range only)
+    const size_t n1 = (size_t)N + 1, nc1 = (size_t)NC + 1;
     const size_t cap = (size_t)std::max<int64_t>(mesh->nnz_bound, 1);
     uint32_t* counters = res->counters.as<uint32_t>();
     FL_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * CNT_WORDS, s));
     if (want_a) {
-        FL_TRY(res->arr[FL_A_COL_PTR].ensure(sizeof(int32_t) * n1));
+        FL_TRY(res->arr[FL_A_COL_PTR].ensure(sizeof(int32_t) * nc1));
         FL_TRY(res->arr[FL_A_ROW_IDX].ensure(sizeof(int32_t) * cap));
         FL_TRY(res->arr[FL_A_VALUES].ensure(sizeof(double) * cap));
-        FL_CUDA(cudaMemsetAsync(res->arr[FL_A_COL_PTR].p, 0, sizeof(int32_t) * n1, s));
+        FL_CUDA(cudaMemsetAsync(res->arr[FL_A_COL_PTR].p, 0, sizeof(int32_t) * nc1, s));
     }
-    if (want_b) FL_TRY(res->arr[FL_B].ensure(sizeof(double) * n1));
+    if (want_b) FL_TRY(res->arr[FL_B].ensure(sizeof(double) * nc1));
     if (want_p) {
         FL_TRY(res->is_dir.ensure(n1));
         FL_TRY(res->is_neu.ensure(n1));
@@ -419,10 +433,10 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         FL_TRY(res->arr[FL_FREE_NODES].ensure(sizeof(int32_t) * n1));
     }
     if (want_sys) {
-        FL_TRY(res->arr[FL_U0].ensure(sizeof(double) * n1));
-        FL_TRY(res->arr[FL_B_MOD].ensure(sizeof(double) * n1));
-        FL_TRY(res->arr[FL_B_F].ensure(sizeof(double) * n1));
-        FL_TRY(res->arr[FL_AFF_COL_PTR].ensure(sizeof(int32_t) * n1));
+        FL_TRY(res->arr[FL_U0].ensure(sizeof(double) * nc1));
+        FL_TRY(res->arr[FL_B_MOD].ensure(sizeof(double) * nc1));
+        FL_TRY(res->arr[FL_B_F].ensure(sizeof(double) * nc1));
+        FL_TRY(res->arr[FL_AFF_COL_PTR].ensure(sizeof(int32_t) * nc1));
         FL_TRY(res->arr[FL_AFF_ROW_IDX].ensure(sizeof(int32_t) * cap));
         FL_TRY(res->arr[FL_AFF_VALUES].ensure(sizeof(double) * cap));
         FL_CUDA(cudaMemsetAsync(res->arr[FL_AFF_COL_PTR].p, 0, sizeof(int32_t), s));
@@ -434,7 +448,9 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         const int tw = column_tile_width();
         p.n_nodes = N;
         p.n_elems = (int32_t)NT;
-        p.n_tiles = (N + tw - 1) / tw;
+        p.c_begin = C0;
+        p.n_cols = NC;
+        p.n_tiles = (NC + tw - 1) / tw;
         FL_TRY(res->tile_status.ensure(sizeof(uint64_t) * ((size_t)p.n_tiles + 1)));
         FL_CUDA(cudaMemsetAsync(res->tile_status.p, 0, sizeof(uint64_t) * ((size_t)p.n_tiles + 1), s));
         p.nodes = mesh->nodes.as<double>();
@@ -461,6 +477,8 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         p.is_dir = res->is_dir.as<int8_t>();
         p.is_neu = res->is_neu.as<int8_t>();
         p.fidx = res->fidx.as<int32_t>();
+        // free nodes below the range = free_rank[C0] (k_partition's exclusive scan)
+        p.f_begin = (C0 > 0 && want_sys) ? res->fidx.as<int32_t>() + n1 + C0 : nullptr;
         p.col_ptr = res->arr[FL_A_COL_PTR].as<int32_t>();
         p.row_idx = res->arr[FL_A_ROW_IDX].as<int32_t>();
         p.values = res->arr[FL_A_VALUES].as<double>();
@@ -484,7 +502,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         x->last = p;
         x->last_mesh = mesh;
         x->last_valid = true;
-        if (N > 0) {
+        if (NC > 0) {
             // v3 (register-centric) by default; v2 (tiled) carries the Dirichlet
             // lift; v1 (general) is the fallback.  FL_KERNEL=1|2|3 forces one.
             const char* kern = std::getenv("FL_KERNEL");
@@ -516,7 +534,15 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
         FL_CUDA(cudaMemcpyAsync(h, res->counters.p, sizeof(uint32_t) * CNT_WORDS,
                                 cudaMemcpyDeviceToHost, s));
         int32_t* hn = reinterpret_cast<int32_t*>(h + CNT_WORDS);
-        hn[0] = hn[1] = 0;
+        hn[0] = hn[1] = hn[2] = hn[3] = hn[4] = 0;
+        const bool sharded_sys = (res->what & FL_OUT_SYSTEM) && res->n != res->m;
+        if (sharded_sys) {  // free nodes before / through the range
+            const int32_t* fr = res->fidx.as<int32_t>() + (size_t)res->m + 1;
+            FL_CUDA(cudaMemcpyAsync(&hn[3], fr + res->col_begin, sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s));
+            FL_CUDA(cudaMemcpyAsync(&hn[4], fr + res->col_begin + res->n, sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, s));
+        }
         if ((res->what & FL_OUT_STIFFNESS) && res->arr[FL_A_COL_PTR].p)
             FL_CUDA(cudaMemcpyAsync(&hn[0], res->arr[FL_A_COL_PTR].as<int32_t>() + res->n,
                                     sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -538,7 +564,8 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
         z.n_neu_faces = (int32_t)h[CNT_NEU_FACES];
         if (res->what & FL_OUT_PARTITION) {
             z.n_dir = (int32_t)h[CNT_N_DIR];
-            z.n_free = res->n - z.n_dir;
+            z.n_free = res->m - z.n_dir;
+            z.n_free_cols = sharded_sys ? hn[4] - hn[3] : z.n_free;
         }
         if (ctx->profile && ctx->timing_pending) {
             float a = 0, b = 0, c = 0;
@@ -568,7 +595,7 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
                 return set_error(FL_E_INVALID_PARAMETER,
                                  "mesh has Dirichlet faces but no g_dirichlet was given");
             int32_t* hf = hn + 2;
-            FL_CUDA(cudaMemcpyAsync(hf, res->arr[FL_AFF_COL_PTR].as<int32_t>() + z.n_free,
+            FL_CUDA(cudaMemcpyAsync(hf, res->arr[FL_AFF_COL_PTR].as<int32_t>() + z.n_free_cols,
                                     sizeof(int32_t), cudaMemcpyDeviceToHost, s));
             FL_CUDA(cudaStreamSynchronize(s));
             z.nnz_ff = *hf;
@@ -591,10 +618,10 @@ static int64_t array_bytes(const fl_result* r, int which) {
     case FL_B_MOD: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n : 0;
     case FL_DIR_NODES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_dir : 0;
     case FL_FREE_NODES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_free : 0;
-    case FL_AFF_COL_PTR: return (r->what & FL_OUT_SYSTEM) ? 4 * ((int64_t)z.n_free + 1) : 0;
+    case FL_AFF_COL_PTR: return (r->what & FL_OUT_SYSTEM) ? 4 * ((int64_t)z.n_free_cols + 1) : 0;
     case FL_AFF_ROW_IDX: return (r->what & FL_OUT_SYSTEM) ? 4 * z.nnz_ff : 0;
     case FL_AFF_VALUES: return (r->what & FL_OUT_SYSTEM) ? 8 * z.nnz_ff : 0;
-    case FL_B_F: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n_free : 0;
+    case FL_B_F: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n_free_cols : 0;
     }
     return -1;
 }
@@ -662,6 +689,7 @@ FL_API int fl_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_pt
     res->what = FL_OUT_STIFFNESS;
     res->n = n_cols;
     res->m = n_rows;
+    res->col_begin = 0;
     res->sizes = fl_sizes{};
     res->sizes.n = n_cols;
     res->sizes.nnz = nnz;

@@ -157,12 +157,13 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
             break;
         }
         if (p.phase_cycles && tid == 0) ph_t = clock64();
-        const int32_t c0 = (int32_t)(tile * TC);
-        const int ncols = min(TC, p.n_nodes - c0);
+        const int32_t lc0 = (int32_t)(tile * TC);  // first owned column of the tile
+        const int32_t c0 = p.c_begin + lc0;         // ... as a global node
+        const int ncols = min(TC, p.n_cols - lc0);
 
         // ---- phase 1: the tile's incidence keys
-        const int32_t base = __ldg(p.inc_ptr + c0);
-        for (int q = tid; q <= TC; q += T::THREADS) ptr[q] = __ldg(p.inc_ptr + c0 + min(q, ncols)) - base;
+        const int32_t base = __ldg(p.inc_ptr + lc0);
+        for (int q = tid; q <= TC; q += T::THREADS) ptr[q] = __ldg(p.inc_ptr + lc0 + min(q, ncols)) - base;
         if (tid == 0) misc[3] = 0;
         __syncthreads();
         const int M = ptr[ncols];
@@ -665,19 +666,20 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
                 }
             }
             if (mine && u == 0) {
-                p.colcnt_a[c] = na[col + 1];
-                if (p.want_sys) p.colcnt_f[c] = nf[col + 1];
+                p.colcnt_a[lc0 + col] = na[col + 1];
+                if (p.want_sys) p.colcnt_f[lc0 + col] = nf[col + 1];
             }
         }
         if (mine && u == 0) {
-            if (p.want_b) p.b[c] = b;
+            const int32_t lc = lc0 + col;
+            if (p.want_b) p.b[lc] = b;
             if (p.want_sys) {
                 const double u0 = p.is_dir[c] ? node_field(p.g_dir, p.nodes, D, c) : 0.0;
                 const double bmod = LIFT ? b - y : b - 0.0;
-                p.u0[c] = u0;
-                p.b_mod[c] = bmod;
+                p.u0[lc] = u0;
+                p.b_mod[lc] = bmod;
                 const int32_t fc = p.fidx[c];
-                if (fc >= 0) p.b_f[fc] = bmod;
+                if (fc >= 0) p.b_f[fc - free_base(p)] = bmod;
             }
         }
         __syncthreads();
@@ -707,8 +709,8 @@ __global__ void k_stage_copy(ColParams p, int tc) {
             p.row_idx[oa + q] = p.st_a_row[sbase + q];
             p.values[oa + q] = p.st_a_val[sbase + q];
         }
-        const int32_t c0 = (int32_t)(t * tc);
-        for (int q = lane; q < tc && c0 + q < p.n_nodes; q += 32)
+        const int32_t c0 = (int32_t)(t * tc);  // local column
+        for (int q = lane; q < tc && c0 + q < p.n_cols; q += 32)
             p.col_ptr[c0 + q + 1] = oa + p.colcnt_a[c0 + q];
         if (p.want_sys) {
             const int32_t of = off_f[t], nf = tot_f[t];
@@ -716,9 +718,10 @@ __global__ void k_stage_copy(ColParams p, int tc) {
                 p.ff_row_idx[of + q] = p.st_f_row[sbase + q];
                 p.ff_values[of + q] = p.st_f_val[sbase + q];
             }
-            for (int q = lane; q < tc && c0 + q < p.n_nodes; q += 32) {
-                const int32_t fc = p.fidx[c0 + q];
-                if (fc >= 0) p.ff_col_ptr[fc + 1] = of + p.colcnt_f[c0 + q];
+            const int32_t fb = free_base(p);
+            for (int q = lane; q < tc && c0 + q < p.n_cols; q += 32) {
+                const int32_t fc = p.fidx[p.c_begin + c0 + q];
+                if (fc >= 0) p.ff_col_ptr[fc - fb + 1] = of + p.colcnt_f[c0 + q];
             }
         }
     }
@@ -747,7 +750,7 @@ static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
 // staging buffers for a tiled launch with `tc` columns and `cap` entries per tile
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap) {
     (void)ctx;
-    p.n_tiles = (p.n_nodes + tc - 1) / tc;
+    p.n_tiles = (p.n_cols + tc - 1) / tc;
     p.tile_cap = cap;
     const size_t nst = (size_t)p.n_tiles * (size_t)p.tile_cap;
     FL_TRY(res->stage[0].ensure(sizeof(int32_t) * nst));
@@ -758,7 +761,7 @@ int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t c
     }
     FL_TRY(res->tile_tot.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_tiles + 1)));
     FL_TRY(res->tile_off.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_tiles + 1)));
-    FL_TRY(res->colcnt.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_nodes + 1)));
+    FL_TRY(res->colcnt.ensure(sizeof(int32_t) * 2 * ((size_t)p.n_cols + 1)));
     p.st_a_row = res->stage[0].as<int32_t>();
     p.st_a_val = res->stage[1].as<double>();
     p.st_f_row = res->stage[2].as<int32_t>();
@@ -766,7 +769,7 @@ int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t c
     p.tile_tot = res->tile_tot.as<int32_t>();
     p.tile_off = res->tile_off.as<int32_t>();
     p.colcnt_a = res->colcnt.as<int32_t>();
-    p.colcnt_f = res->colcnt.as<int32_t>() + p.n_nodes + 1;
+    p.colcnt_f = res->colcnt.as<int32_t>() + p.n_cols + 1;
     return FL_OK;
 }
 

@@ -11,17 +11,18 @@
 //   2. each lane computes its element's column j: s_ij (i = 0..d) and the load
 //      share (fl_geometry.cuh, FMA-free, exact division);
 //   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
-//      A(c,c) = fold of s_jj in lane order (its items are exactly those), both
-//      by shuffles;
+//      A(c,c) = fold of s_jj in lane order (its items are exactly those): the
+//      shares are staged in smem and group lanes 0 / 1 run the two folds;
 //   4. off-diagonal items (i != j): per pass i, lanes with the same row are found
 //      with match_any; the pass's group leader inserts the row in the group's
-//      small smem hash (CAS) and broadcasts the slot; the items are then added
-//      to the slot accumulator in rounds of increasing lane rank, so every slot
-//      sums its items in (i, then lane) order = the reference's (i*(d+1)+j, t);
+//      small smem hash (CAS), reserves popc(match) positions in the slot's item
+//      list and broadcasts (slot, first position); each item stores itself at
+//      first + rank-in-match.  A slot's list is thus in (i, then lane) order =
+//      the reference's (i*(d+1)+j, t); one lane per slot then folds its list;
 //   5. slots ranked by row, exact zeros dropped (sparse.hpp:105), A(free,free)
 //      rows kept, all written to the tile staging (k_stage_copy places them).
-// Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, or
-// more distinct rows than the group table holds.
+// Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, more
+// distinct rows than the group table holds, or more than CAP items on one row.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -40,6 +41,7 @@ struct V3 {
     static constexpr int GPW = 32 / L;                 // column groups per warp
     static constexpr int HS = D == 2 ? 16 : 32;        // slot table entries per group
     static constexpr int MAXS = D == 2 ? 12 : 24;      // distinct rows accepted per column
+    static constexpr int CAP = D == 2 ? 8 : 16;        // items per off-diagonal row
     static constexpr int WTC = D == 2 ? 32 : 8;        // columns per warp tile
     static constexpr int ITERS = WTC / GPW;            // group iterations per warp tile
     static constexpr int WARPS = 4;                    // warps per CTA
@@ -47,10 +49,12 @@ struct V3 {
 
 template <int D, int L>
 struct V3Smem {  // one per group
-    int32_t row[V3<D, L>::HS];
-    double acc[V3<D, L>::HS];
-    int32_t srow[V3<D, L>::HS];
+    alignas(16) int32_t row[V3<D, L>::HS];  // slot -> row (-1 empty)
+    int32_t cnt[V3<D, L>::HS];              // slot -> items listed
+    int32_t srow[V3<D, L>::HS];             // rows in ascending order
     double sval[V3<D, L>::HS];
+    double lb[L], ld[L];                    // load shares / s_jj in lane order
+    double item[V3<D, L>::CAP][V3<D, L>::HS];  // per-slot item lists, position-major
 };
 
 __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* nodes, int dim,
@@ -86,12 +90,13 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
         int run_a = 0, run_f = 0;  // warp-uniform: entries staged so far in this tile
         bool bad = false;
         for (int it = 0; it < C::ITERS; ++it) {
-            const int32_t c = (int32_t)(tile * C::WTC) + it * C::GPW + gi;
-            const bool act = c < p.n_nodes;
+            const int32_t lc = (int32_t)(tile * C::WTC) + it * C::GPW + gi;  // owned column
+            const bool act = lc < p.n_cols;
+            const int32_t c = p.c_begin + lc;  // global node
             int32_t p0 = 0, m = 0;
             if (act) {
-                p0 = __ldg(p.inc_ptr + c);
-                m = __ldg(p.inc_ptr + c + 1) - p0;
+                p0 = __ldg(p.inc_ptr + lc);
+                m = __ldg(p.inc_ptr + lc + 1) - p0;
             }
             if (m > L) {
                 bad = true;
@@ -154,20 +159,23 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
                 for (int i = 0; i < NV; ++i)
                     if (i == j) sjj = s[i];
             }
-            // ---- 3. b and the diagonal: sequential folds in lane order
-            double b = 0.0, dg = -0.0;
-            const int mmax = __reduce_max_sync(FULL, (unsigned)m);
-            for (int q = 0; q < mmax; ++q) {
-                const double lq = __shfl_sync(FULL, l, q, L);
-                const double sq = __shfl_sync(FULL, sjj, q, L);
-                if (q < m) {
-                    b = b + lq;
-                    dg = dg + sq;
-                }
+            // ---- 3. b and the diagonal: sequential folds in lane order (lanes 0 / 1)
+            sm.lb[g] = l;
+            sm.ld[g] = sjj;
+            __syncwarp();
+            double fold = g == 0 ? 0.0 : -0.0;
+            if (g < 2) {
+                const double* src = g == 0 ? sm.lb : sm.ld;
+                for (int q = 0; q < m; ++q) fold = fold + src[q];
             }
-            // ---- 4. off-diagonal slots and their ordered folds
+            const double b = __shfl_sync(FULL, fold, 0, L);
+            const double dg = __shfl_sync(FULL, fold, 1, L);
+            // ---- 4. off-diagonal items into per-row lists in (i, lane) order
             if (p.want_a) {
-                for (int h = g; h < C::HS; h += L) sm.row[h] = -1;
+                for (int h = g; h < C::HS; h += L) {
+                    sm.row[h] = -1;
+                    sm.cnt[h] = 0;
+                }
                 __syncwarp();
                 int nslot = 0;
 #pragma unroll
@@ -177,40 +185,41 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
                                             : ((1ull << 63) | (uint64_t)lane);
                     const unsigned gm = __match_any_sync(FULL, mk);
                     const int rank = __popc(gm & lower);
-                    int slot = -1;
+                    int sb = -1;  // slot | first position << 8
                     if (has && rank == 0) {
                         const int32_t r = R[i];
                         uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                        int slot = -1;
                         for (int probe = 0; probe < C::HS; ++probe) {
                             const int32_t old = atomicCAS(&sm.row[h], -1, r);
-                            if (old == -1) {
-                                sm.acc[h] = -0.0;  // -0.0 + x == x: the fold starts at its first value
-                                slot = (int)h;
-                                break;
-                            }
-                            if (old == r) {
+                            if (old == -1 || old == r) {
                                 slot = (int)h;
                                 break;
                             }
                             h = (h + 1) & (C::HS - 1);
                         }
-                        if (slot < 0) bad = true;
+                        if (slot >= 0) {
+                            const int f0 = sm.cnt[slot];
+                            sm.cnt[slot] = f0 + __popc(gm);
+                            sb = slot | (f0 << 8);
+                        } else {
+                            bad = true;
+                        }
                     }
-                    slot = __shfl_sync(FULL, slot, __ffs(gm) - 1);
+                    sb = __shfl_sync(FULL, sb, __ffs(gm) - 1);
+                    if (has && sb >= 0) {
+                        const int pos = (sb >> 8) + rank;
+                        if (pos < C::CAP) sm.item[pos][sb & 0xFF] = s[i];
+                        else bad = true;
+                    }
                     __syncwarp();
-                    const int rounds = __reduce_max_sync(FULL, has ? (unsigned)__popc(gm) : 0u);
-                    for (int rr = 0; rr < rounds; ++rr) {
-                        if (has && rank == rr && slot >= 0) sm.acc[slot] = sm.acc[slot] + s[i];
-                        __syncwarp();
-                    }
                 }
-                // ---- 5. rows in ascending order (diagonal included), zero drop
+                // ---- 5. fold each row's list (one lane per slot), rank rows, zero drop
                 if (g == 0 && act && m > 0) {
                     uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
                     for (int probe = 0; probe < C::HS; ++probe) {
                         if (sm.row[h] == -1) {
                             sm.row[h] = c;
-                            sm.acc[h] = dg;
                             break;
                         }
                         h = (h + 1) & (C::HS - 1);
@@ -220,15 +229,23 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
                 for (int h = g; h < C::HS; h += L) {
                     const int32_t r = sm.row[h];
                     if (r >= 0) {
-                        int rk = 0;
-#pragma unroll 8
-                        for (int q = 0; q < C::HS; ++q) {
-                            const int32_t rq = sm.row[q];
-                            rk += (rq >= 0) & (rq < r);
+                        double acc = dg;
+                        if (r != c) {
+                            acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                            const int n = min(sm.cnt[h], C::CAP);
+                            for (int k = 0; k < n; ++k) acc = acc + sm.item[k][h];
+                        }
+                        int rk = 0;  // rows below r; empty slots (-1) compare as huge
+                        const int4* r4 = reinterpret_cast<const int4*>(sm.row);
+#pragma unroll
+                        for (int q = 0; q < C::HS / 4; ++q) {
+                            const int4 v = r4[q];
+                            rk += ((uint32_t)v.x < (uint32_t)r) + ((uint32_t)v.y < (uint32_t)r) +
+                                  ((uint32_t)v.z < (uint32_t)r) + ((uint32_t)v.w < (uint32_t)r);
                         }
                         if (rk < C::MAXS) {
                             sm.srow[rk] = r;
-                            sm.sval[rk] = sm.acc[h];
+                            sm.sval[rk] = acc;
                         }
                     }
                 }
@@ -269,8 +286,8 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
                 const int tot_a = __shfl_sync(FULL, pa, 31), tot_f = __shfl_sync(FULL, pf, 31);
                 int wa = run_a + pa - na, wf = run_f + pf - nf;  // this column's first slot
                 if (act && g == 0) {
-                    p.colcnt_a[c] = wa + na;
-                    if (p.want_sys) p.colcnt_f[c] = wf + nf;
+                    p.colcnt_a[lc] = wa + na;
+                    if (p.want_sys) p.colcnt_f[lc] = wf + nf;
                 }
                 // pass 2: write
                 for (int base = 0; base < C::MAXS; base += L) {
@@ -302,14 +319,14 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
             }
             // ---- per-column vectors
             if (act && g == 0) {
-                if (p.want_b) p.b[c] = b;
+                if (p.want_b) p.b[lc] = b;
                 if (p.want_sys) {
                     const double u0 = p.is_dir[c] ? node_field3(p.g_dir, p.nodes, D, c) : 0.0;
                     const double bmod = b - 0.0;  // no lift on this path (g == 0)
-                    p.u0[c] = u0;
-                    p.b_mod[c] = bmod;
+                    p.u0[lc] = u0;
+                    p.b_mod[lc] = bmod;
                     const int32_t fc = p.fidx[c];
-                    if (fc >= 0) p.b_f[fc] = bmod;
+                    if (fc >= 0) p.b_f[fc - free_base(p)] = bmod;
                 }
             }
         }

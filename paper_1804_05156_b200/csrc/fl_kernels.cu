@@ -25,8 +25,9 @@ namespace fl {
 // ===========================================================================
 // plan
 // ===========================================================================
-__global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ elems,
-                            int32_t* __restrict__ cnt, uint32_t* __restrict__ err) {
+__global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
+                            const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ err) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = __ldg(elems + e);
@@ -34,11 +35,12 @@ __global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, const int32_t* _
             atomicOr(err, DERR_INDEX);
             continue;
         }
-        atomicAdd(cnt + v, 1);
+        const uint32_t lv = (uint32_t)(v - c_begin);
+        if (lv < (uint32_t)n_cols) atomicAdd(cnt + lv, 1);
     }
 }
 
-__global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes,
+__global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
                            const int32_t* __restrict__ elems, const int32_t* __restrict__ inc_ptr,
                            int32_t* __restrict__ cursor, uint32_t* __restrict__ inc) {
     const int64_t n_entries = (int64_t)n_elems * nv;
@@ -46,9 +48,11 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes,
          e += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = __ldg(elems + e);
         if (v < 0 || v >= n_nodes) continue;
+        const uint32_t lv = (uint32_t)(v - c_begin);
+        if (lv >= (uint32_t)n_cols) continue;
         const int32_t t = (int32_t)(e / nv);
         const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
-        const int32_t pos = __ldg(inc_ptr + v) + atomicAdd(cursor + v, 1);
+        const int32_t pos = __ldg(inc_ptr + lv) + atomicAdd(cursor + lv, 1);
         inc[pos] = (j << 30) | (uint32_t)t;
     }
 }
@@ -72,11 +76,12 @@ __global__ void k_inc_sort(int32_t n_nodes, const int32_t* __restrict__ inc_ptr,
 }
 
 // stats[0] += sum_c min(m_c * d + 1, N)  (nnz upper bound), stats[1] = max m_c
-__global__ void k_plan_stats(int32_t n_nodes, int dim, const int32_t* __restrict__ inc_ptr,
+__global__ void k_plan_stats(int32_t n_cols, int32_t n_nodes, int dim,
+                             const int32_t* __restrict__ inc_ptr,
                              unsigned long long* __restrict__ stats) {
     int64_t bound = 0;
     int32_t mx = 0;
-    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_nodes;
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cols;
          c += gridDim.x * blockDim.x) {
         const int32_t m = inc_ptr[c + 1] - inc_ptr[c];
         const int64_t b = (int64_t)m * dim + 1;
@@ -346,8 +351,8 @@ template <int D>
 __device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lane,
                             double& b_out, double& bmod_out, double& u0_out) {
     const unsigned FULL = 0xffffffffu;
-    const int32_t p0 = p.inc_ptr[c];
-    const int32_t m = p.inc_ptr[c + 1] - p0;
+    const int32_t p0 = p.inc_ptr[c - p.c_begin];
+    const int32_t m = p.inc_ptr[c - p.c_begin + 1] - p0;
     const int nchunks = (m + 31) >> 5;
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
@@ -595,9 +600,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
         __syncthreads();
         const int64_t tile = s_tile;
         if (tile >= p.n_tiles) break;
-        const int64_t c64 = tile * kWarps + w;
-        const bool has = c64 < p.n_nodes;
-        const int32_t c = (int32_t)c64;
+        const int64_t lc64 = tile * kWarps + w;
+        const bool has = lc64 < p.n_cols;
+        const int32_t lc = (int32_t)lc64, c = p.c_begin + lc;
         double b = 0.0, bmod = 0.0, u0 = 0.0;
         if (has) {
             column_warp<D>(p, c, ws, lane, b, bmod, u0);
@@ -636,9 +641,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
                         p.row_idx[off_a + q] = ws.out_rows[q];
                         p.values[off_a + q] = ws.out_vals[q];
                     }
-                    if (lane == 0) p.col_ptr[c + 1] = (int32_t)(off_a + na);
+                    if (lane == 0) p.col_ptr[lc + 1] = (int32_t)(off_a + na);
                     if (p.want_sys) {
-                        const int32_t fc = p.fidx[c];
+                        const int32_t fc = p.fidx[c] - free_base(p);
                         for (int q = lane; q < nf; q += 32) {
                             p.ff_row_idx[off_f + q] = ws.ff_rows[q];
                             p.ff_values[off_f + q] = ws.ff_vals[q];
@@ -648,12 +653,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
                 }
             }
             if (lane == 0) {
-                if (p.want_b) p.b[c] = b;
+                if (p.want_b) p.b[lc] = b;
                 if (p.want_sys) {
-                    p.u0[c] = u0;
-                    p.b_mod[c] = bmod;
+                    p.u0[lc] = u0;
+                    p.b_mod[lc] = bmod;
                     const int32_t fc = p.fidx[c];
-                    if (fc >= 0) p.b_f[fc] = bmod;
+                    if (fc >= 0) p.b_f[fc - free_base(p)] = bmod;
                 }
             }
         }
@@ -738,34 +743,35 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
     const int nv = mesh->dim + 1;
     const int64_t n_entries = (int64_t)mesh->n_elems * nv;
     const int32_t N = mesh->n_nodes;
-    FL_TRY(mesh->inc_ptr.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-    FL_TRY(mesh->cursor.ensure(sizeof(int32_t) * ((size_t)N + 1)));
+    const int32_t c0 = mesh->col_begin, nc = mesh->col_end - mesh->col_begin;
+    FL_TRY(mesh->inc_ptr.ensure(sizeof(int32_t) * ((size_t)nc + 1)));
+    FL_TRY(mesh->cursor.ensure(sizeof(int32_t) * ((size_t)nc + 1)));
     FL_TRY(mesh->inc.ensure(sizeof(uint32_t) * (size_t)(n_entries > 0 ? n_entries : 1)));
     FL_TRY(mesh->stats.ensure(sizeof(unsigned long long) * 4));
-    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(N)));
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(nc)));
     int32_t* cnt = mesh->cursor.as<int32_t>();
-    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)nc + 1), s));
     FL_CUDA(cudaMemsetAsync(mesh->stats.p, 0, sizeof(unsigned long long) * 4, s));
     const int grid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256), 1),
                                             (int64_t)ctx->sm_count * 16);
     if (n_entries > 0) {
-        k_inc_count<<<grid, 256, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, d_err);
+        k_inc_count<<<grid, 256, 0, s>>>(n_entries, N, c0, nc, mesh->elems.as<int32_t>(), cnt, d_err);
         count_launch(ctx);
     }
     const int32_t* cnt_c = cnt;
     FL_CUDA(launch_scan<int32_t>(
-        N, [cnt_c] __device__(int64_t i) { return (int64_t)cnt_c[i]; },
+        nc, [cnt_c] __device__(int64_t i) { return (int64_t)cnt_c[i]; },
         mesh->inc_ptr.as<int32_t>(), ctx->scan_ws.p, s));
     count_launch(ctx);
-    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)nc + 1), s));
     if (n_entries > 0) {
-        k_inc_fill<<<grid, 256, 0, s>>>(mesh->n_elems, nv, N, mesh->elems.as<int32_t>(),
+        k_inc_fill<<<grid, 256, 0, s>>>(mesh->n_elems, nv, N, c0, nc, mesh->elems.as<int32_t>(),
                                         mesh->inc_ptr.as<int32_t>(), cnt, mesh->inc.as<uint32_t>());
         count_launch(ctx);
     }
-    if (N > 0) {
-        k_plan_stats<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(
-            N, mesh->dim, mesh->inc_ptr.as<int32_t>(), mesh->stats.as<unsigned long long>());
+    if (nc > 0) {
+        k_plan_stats<<<std::min(div_up(nc, 256), ctx->sm_count * 8), 256, 0, s>>>(
+            nc, N, mesh->dim, mesh->inc_ptr.as<int32_t>(), mesh->stats.as<unsigned long long>());
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
@@ -775,10 +781,10 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
 // The general kernel needs each node's incidences in (j, t) order; the tiled
 // kernel ranks them itself, so this pass only runs on the fallback path.
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh) {
-    const int32_t N = mesh->n_nodes;
-    if (N > 0) {
-        k_inc_sort<<<div_up(N, 128), 128, 0, ctx->stream>>>(N, mesh->inc_ptr.as<int32_t>(),
-                                                           mesh->inc.as<uint32_t>());
+    const int32_t nc = mesh->col_end - mesh->col_begin;
+    if (nc > 0) {
+        k_inc_sort<<<div_up(nc, 128), 128, 0, ctx->stream>>>(nc, mesh->inc_ptr.as<int32_t>(),
+                                                            mesh->inc.as<uint32_t>());
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());

@@ -10,6 +10,12 @@ namespace fl {
 
 struct ColParams {
     int32_t n_nodes, n_elems;
+    // owned columns [c_begin, c_begin + n_cols).  Column-indexed inputs (is_dir,
+    // fidx, node fields) use the global column c; the plan (inc_ptr) and the
+    // column outputs (col_ptr, b, u0, b_mod, colcnt_*) use lc = c - c_begin, and
+    // A(free, free) columns / b_f use fidx[c] - *f_begin (free nodes below c_begin).
+    int32_t c_begin, n_cols;
+    const int32_t* f_begin;  // device scalar, nullptr = 0
     int64_t n_tiles;
     const double* nodes;
     const int32_t* elems;
@@ -48,6 +54,10 @@ struct ColParams {
     int32_t* colcnt_a;   // [N] in-tile inclusive count after column c
     int32_t* colcnt_f;   // [N] same for A(free, free) (indexed by column c)
 };
+
+__device__ __forceinline__ int32_t free_base(const ColParams& p) {
+    return p.f_begin ? __ldg(p.f_begin) : 0;
+}
 
 int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);
 int launch_validate(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err);

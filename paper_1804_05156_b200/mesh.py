@@ -91,6 +91,11 @@ class DeviceMesh:
     def handle(self):
         return self._h
 
+    def set_columns(self, col_begin: int, col_end: int):
+        """Own CSC columns [col_begin, col_end) only (one rank's shard)."""
+        _lib.check(_lib.lib().fl_mesh_set_columns(self.ctx.handle, self._h, int(col_begin),
+                                                  int(col_end)), "fl_mesh_set_columns")
+
     def plan(self):
         _lib.check(_lib.lib().fl_mesh_plan(self.ctx.handle, self._h), "fl_mesh_plan")
 

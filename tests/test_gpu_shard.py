@@ -1,0 +1,120 @@
+"""GPU: the B200 path against the reference's golden fixtures, and the
+column-sharded (multi-GPU) path against the unsharded one.
+
+Sharding runs every rank's column range on the one GPU in turn (no rank waits
+on another: the ranks are independent by construction); the
+stitched shards must equal the reference's single CSC bit for bit, for each
+column kernel (FL_KERNEL=1 general, 2 tiled, 3 register-centric).
+"""
+from __future__ import annotations
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_1804_05156_b200 as fl
+from paper_1804_05156_b200 import _lib
+from paper_1804_05156_b200.mesh import Mesh
+from paper_1804_05156_b200.shard import ShardedAssembler, column_ranges, exclusive_offsets, stitch_csc
+
+pytestmark = pytest.mark.gpu
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+IDS = [os.path.basename(p)[:-4] for p in GOLDEN]
+
+
+def _mesh(g):
+    return Mesh(int(g["dim"]), g["nodes"], g["elems"], g["flags"])
+
+
+def _bits(x):
+    return np.asarray(x, dtype=np.float64).tobytes()
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=IDS)
+def test_gpu_matches_golden(path, ctx):
+    g = np.load(path)
+    m = _mesh(g)
+    a = fl.assemble_blockwise(m, ctx=ctx)
+    np.testing.assert_array_equal(a.col_ptr, g["a_col_ptr"])
+    np.testing.assert_array_equal(a.row_idx, g["a_row_idx"])
+    assert _bits(a.values) == _bits(g["a_values"])
+    ac = fl.assemble_blockwise(m, coef=g["coef"], ctx=ctx)
+    np.testing.assert_array_equal(ac.col_ptr, g["ac_col_ptr"])
+    assert _bits(ac.values) == _bits(g["ac_values"])
+    for kind, spec in [(1, 1.0), (3, "x"), (4, "xyz")]:
+        assert _bits(fl.assemble_load(m, spec, ctx=ctx)) == _bits(g[f"b_{kind}"]), kind
+    p = fl.partition_boundary(m, ctx=ctx)
+    np.testing.assert_array_equal(p.dirichlet_nodes, g["dir_nodes"])
+    np.testing.assert_array_equal(p.free_nodes, g["free_nodes"])
+    if g["dir_nodes"].size:
+        s = fl.poisson_system(m, 1.0, "x", ctx=ctx)
+        assert _bits(s.u0) == _bits(g["u0_x"])
+        assert _bits(s.b_mod) == _bits(g["bmod_x"])
+        np.testing.assert_array_equal(s.a_ff.col_ptr, g["aff_col_ptr"])
+        np.testing.assert_array_equal(s.a_ff.row_idx, g["aff_row_idx"])
+        assert _bits(s.a_ff.values) == _bits(g["aff_values"])
+    if np.any(g["flags"] == 2):
+        r = fl.run(m, _lib.OUT_LOAD | _lib.OUT_PARTITION, f=1.0, g_neumann=1.5, ctx=ctx)
+        assert _bits(r.vector(_lib.B)) == _bits(g["b_neumann_const15"])
+
+
+def _shards(m, world, what, ctx, **fields):
+    out = []
+    for r in range(world):
+        sa = ShardedAssembler(m, r, world, ctx=ctx)
+        res = sa.assemble(what, **fields)
+        out.append((sa, res, sa.local_counts(res)))
+    return out
+
+
+@pytest.mark.parametrize("kernel", ["1", "2", "3"])
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("tag", ["square8_jit", "cube3_mixed_jit", "lshape4_jit"])
+def test_sharded_stiffness_and_load(tag, world, kernel, ctx, monkeypatch):
+    monkeypatch.setenv("FL_KERNEL", kernel)
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", tag + ".npz"))
+    m = _mesh(g)
+    parts = _shards(m, world, _lib.OUT_STIFFNESS | _lib.OUT_LOAD, ctx, f=1.0)
+    full = stitch_csc(m.num_nodes(), [(r.matrix().col_ptr, r.matrix().row_idx, r.matrix().values)
+                                      for _, r, _ in parts])
+    np.testing.assert_array_equal(full.col_ptr, g["a_col_ptr"])
+    np.testing.assert_array_equal(full.row_idx, g["a_row_idx"])
+    assert _bits(full.values) == _bits(g["a_values"])
+    b = np.concatenate([r.vector(_lib.B) for _, r, _ in parts])
+    assert _bits(b) == _bits(g["b_1"])
+    off = exclusive_offsets(np.asarray([c for _, _, c in parts]))
+    for k, (c0, _) in enumerate(column_ranges(m.num_nodes(), world)):
+        assert off[k, 2] == g["a_col_ptr"][c0]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("gspec", [0.0, "x"])
+@pytest.mark.parametrize("tag", ["square8_jit", "cube3_mixed_jit"])
+def test_sharded_system(tag, gspec, world, ctx):
+    """A(free, free), b_f, u0, b_mod split by column range (lift path included)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", tag + ".npz"))
+    m = _mesh(g)
+    ref = fl.poisson_system(m, 1.0, gspec, ctx=ctx)
+    parts = _shards(m, world, _lib.OUT_SYSTEM, ctx, f=1.0, g_dirichlet=gspec)
+    aff = stitch_csc(ref.a_ff.m, [(r.matrix_ff().col_ptr, r.matrix_ff().row_idx,
+                                   r.matrix_ff().values) for _, r, _ in parts])
+    np.testing.assert_array_equal(aff.col_ptr, ref.a_ff.col_ptr)
+    np.testing.assert_array_equal(aff.row_idx, ref.a_ff.row_idx)
+    assert _bits(aff.values) == _bits(ref.a_ff.values)
+    for which, full in [(_lib.U0, ref.u0), (_lib.B_MOD, ref.b_mod), (_lib.B_F, ref.b_f),
+                        (_lib.B, ref.b)]:
+        got = np.concatenate([r.vector(which) for _, r, _ in parts])
+        assert _bits(got) == _bits(full), which
+    for _, r, _ in parts:  # the partition outputs stay global
+        np.testing.assert_array_equal(r.partition().free_nodes, ref.partition.free_nodes)
+
+
+def test_set_columns_rejects_bad_range(ctx):
+    g = np.load(GOLDEN[0])
+    dm = _mesh(g).device(ctx)
+    with pytest.raises(fl.Error):
+        dm.set_columns(2, 1)
+    with pytest.raises(fl.Error):
+        dm.set_columns(0, g["nodes"].shape[0] + 1)
