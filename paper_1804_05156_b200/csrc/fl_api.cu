@@ -355,6 +355,11 @@ FL_API int fl_result_destroy(fl_result* r) {
     r->is_neu.release();
     r->fidx.release();
     r->tile_status.release();
+    for (auto& b : r->stage) b.release();
+    r->tile_tot.release();
+    r->tile_off.release();
+    r->colcnt.release();
+    for (auto& b : r->erec) b.release();
     r->counters.release();
     fl_result_ext* x = ext_of(r);
     x->stage.f.release();
@@ -503,8 +508,9 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         x->last_mesh = mesh;
         x->last_valid = true;
         if (NC > 0) {
-            // v3 (register-centric) by default; v2 (tiled) carries the Dirichlet
-            // lift; v1 (general) is the fallback.  FL_KERNEL=1|2|3 forces one.
+            // element records + v3 (register-centric) by default; v2 (tiled)
+            // carries the Dirichlet lift; v1 (general) is the fallback.
+            // FL_KERNEL=1|2|3 forces one (3 = v3 with in-kernel geometry).
             const char* kern = std::getenv("FL_KERNEL");
             const char k = kern ? kern[0] : '0';
             if (k == '1') {
@@ -513,7 +519,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             } else if (k == '2' || p.need_lift || (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)) {
                 FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
             } else {
-                FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res));
+                FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res, k != '3'));
             }
         }
     }

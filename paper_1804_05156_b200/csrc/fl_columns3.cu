@@ -67,8 +67,91 @@ __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* 
     return eval_point(g, x, y, z);
 }
 
-template <int D, int L>
-__global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) {
+// Element-first records: one thread per element computes the whole local
+// matrix (stiffness_all: the same operations as stiffness_col, s_ij == s_ji)
+// times the coefficient, and the load shares of its D+1 vertices, once --
+// instead of once per incident column.
+constexpr int kElemThreads = 128;
+
+template <int D>
+__global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
+    constexpr int NV = D + 1;
+    constexpr int W = NV * 4 + 1;  // int4 words per element in smem (+1: no bank conflicts)
+    __shared__ int4 stage[kElemThreads * W];
+    const Recip R3 = recip(3.0);
+    const Recip R6 = recip(6.0);
+    for (int64_t t0 = (int64_t)blockIdx.x * kElemThreads; t0 < p.n_elems;
+         t0 += (int64_t)gridDim.x * kElemThreads) {
+        const int64_t t = t0 + threadIdx.x;
+        if (t < p.n_elems) {
+            int32_t V[NV];
+            if constexpr (D == 3) {
+                const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
+                V[0] = e.x;
+                V[1] = e.y;
+                V[2] = e.z;
+                V[3] = e.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < NV; ++i) V[i] = __ldg(p.elems + (size_t)t * NV + i);
+            }
+            ElemCol<D> ec;
+            ec.load(p.nodes, V);
+            double S[NV][NV];
+            double meas;
+            if constexpr (D == 2) meas = ec.stiffness_all(S);
+            else meas = ec.stiffness_all(S, R6);
+            if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
+            if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
+                double a;
+                if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
+                else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t);
+                else a = ec.coef_c5(R3);
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) S[j][i] = S[j][i] * a;
+            }
+            double Lj[NV];
+            if constexpr (D == 2) {
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+                    Lj[j] = p.want_b ? ec.load_col(j, (int32_t)t, p.f, R6) : 0.0;
+            } else {
+                if (p.want_b) ec.load_all((int32_t)t, meas, p.f, Lj);
+                else Lj[0] = Lj[1] = Lj[2] = Lj[3] = 0.0;
+            }
+            // one 64-byte record per incidence (t, j): column j of the local matrix
+            // (= row j by symmetry), the load share, the vertices
+            int4* st = stage + threadIdx.x * W;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                double2 w0 = make_double2(S[j][0], S[j][1]);
+                double2 w1 = D == 3 ? make_double2(S[j][2], S[j][3]) : make_double2(S[j][2], Lj[j]);
+                double2 w2 = D == 3 ? make_double2(Lj[j], 0.0) : make_double2(0.0, 0.0);
+                st[4 * j] = *reinterpret_cast<int4*>(&w0);
+                st[4 * j + 1] = *reinterpret_cast<int4*>(&w1);
+                if constexpr (D == 3) {
+                    st[4 * j + 2] = *reinterpret_cast<int4*>(&w2);
+                    st[4 * j + 3] = make_int4(V[0], V[1], V[2], V[3]);
+                } else {
+                    st[4 * j + 2] = make_int4(V[0], V[1], V[2], 0);
+                    st[4 * j + 3] = make_int4(0, 0, 0, 0);
+                }
+            }
+        }
+        __syncthreads();
+        // coalesced write-out of the block's contiguous records
+        const int64_t n = min((int64_t)kElemThreads, p.n_elems - t0);
+        int4* out = reinterpret_cast<int4*>(p.srec) + t0 * NV * 4;
+        for (int q = threadIdx.x; q < n * NV * 4; q += kElemThreads)
+            out[q] = stage[(q / (NV * 4)) * W + q % (NV * 4)];
+        __syncthreads();
+    }
+}
+
+template <int D, int L, bool PRE>
+__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(ColParams p) {
     using C = V3<D, L>;
     constexpr int NV = D + 1;
     constexpr unsigned FULL = 0xffffffffu;
@@ -126,7 +209,29 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
                 R[i] = -1;
                 s[i] = 0.0;
             }
-            if (valid) {
+            if (valid && PRE) {
+                const double2* rec =
+                    reinterpret_cast<const double2*>(p.srec + ((size_t)t * NV + j) * 8);
+                const double2 a01 = __ldg(rec), a23 = __ldg(rec + 1);
+                s[0] = a01.x;
+                s[1] = a01.y;
+                s[2] = a23.x;
+                if constexpr (D == 3) {
+                    s[3] = a23.y;
+                    l = __ldg(rec + 2).x;
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 3);
+                    R[0] = e.x;
+                    R[1] = e.y;
+                    R[2] = e.z;
+                    R[3] = e.w;
+                } else {
+                    l = a23.y;
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 2);
+                    R[0] = e.x;
+                    R[1] = e.y;
+                    R[2] = e.z;
+                }
+            } else if (valid) {
                 if constexpr (D == 3) {
                     const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
                     R[0] = e.x;
@@ -137,24 +242,28 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
 #pragma unroll
                     for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t * NV + i);
                 }
-                ElemCol<D> ec;
-                ec.load(p.nodes, R);
-                double meas;
-                if constexpr (D == 2) meas = ec.stiffness_col(j, s);
-                else meas = ec.stiffness_col(j, s, R6);
-                if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
-                if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
-                    double a;
-                    if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
-                    else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t);
-                    else a = ec.coef_c5(R3);
+                {
+                    ElemCol<D> ec;
+                    ec.load(p.nodes, R);
+                    double meas;
+                    if constexpr (D == 2) meas = ec.stiffness_col(j, s);
+                    else meas = ec.stiffness_col(j, s, R6);
+                    if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
+                    if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
+                        double a;
+                        if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
+                        else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t);
+                        else a = ec.coef_c5(R3);
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) s[i] = s[i] * a;
+                        for (int i = 0; i < NV; ++i) s[i] = s[i] * a;
+                    }
+                    if (p.want_b) {
+                        if constexpr (D == 2) l = ec.load_col(j, t, p.f, R6);
+                        else l = ec.load_col(j, t, meas, p.f);
+                    }
                 }
-                if (p.want_b) {
-                    if constexpr (D == 2) l = ec.load_col(j, t, p.f, R6);
-                    else l = ec.load_col(j, t, meas, p.f);
-                }
+            }
+            if (valid) {
 #pragma unroll
                 for (int i = 0; i < NV; ++i)
                     if (i == j) sjj = s[i];
@@ -338,28 +447,41 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32) k_columns3(ColParams p) 
     }
 }
 
-template <int D, int L>
+template <int D, int L, bool PRE>
 static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     using C = V3<D, L>;
     FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
+    if constexpr (PRE) {
+        const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
+        FL_TRY(res->erec[0].ensure((size_t)64 * ne * (D + 1)));
+        p.srec = res->erec[0].as<double>();
+        p.lrec = nullptr;
+        if (p.n_elems > 0) {
+            const int g = std::min(div_up(p.n_elems, kElemThreads), ctx->sm_count * 16);
+            k_elem_records<D><<<g, kElemThreads, 0, ctx->stream>>>(p);
+            count_launch(ctx);
+        }
+    }
     int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L>, C::WARPS * 32, 0));
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE>,
+                                                          C::WARPS * 32, 0));
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS,
                              (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    k_columns3<D, L><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
+    k_columns3<D, L, PRE><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return finish_staging(ctx, p, C::WTC);
 }
 
-// kmax: the plan's largest node valence; need_lift meshes use the tiled kernel
-int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res) {
+// kmax: the plan's largest node valence; need_lift meshes use the tiled kernel.
+// pre: element-first records (default) or per-incidence geometry in the kernel.
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre) {
     if (dim == 2) {
-        if (kmax <= 8) return launch3<2, 8>(ctx, p, res);
-        return launch3<2, 16>(ctx, p, res);
+        if (kmax <= 8) return pre ? launch3<2, 8, true>(ctx, p, res) : launch3<2, 8, false>(ctx, p, res);
+        return pre ? launch3<2, 16, true>(ctx, p, res) : launch3<2, 16, false>(ctx, p, res);
     }
-    return launch3<3, 32>(ctx, p, res);
+    return pre ? launch3<3, 32, true>(ctx, p, res) : launch3<3, 32, false>(ctx, p, res);
 }
 
 }  // namespace fl

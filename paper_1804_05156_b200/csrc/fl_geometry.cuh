@@ -72,6 +72,24 @@ struct ElemCol<2> {
         return area;
     }
 
+    // the whole local matrix at once (element-first path): s_ij for all i, j with
+    // exactly stiffness_col's operations; the dot product is symmetric in (i, j)
+    // operand for operand, so s_ij == s_ji bitwise and only i <= j is computed
+    __device__ __forceinline__ double stiffness_all(double s[3][3]) const {
+        const double ex[3] = {x[2] - x[1], x[0] - x[2], x[1] - x[0]};
+        const double ey[3] = {y[2] - y[1], y[0] - y[2], y[1] - y[0]};
+        const double area = 0.5 * fabs(-ex[2] * ey[1] + ey[2] * ex[1]);
+        const Recip R = recip(4.0 * area);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i <= j; ++i) {
+                const double dot = (-ey[i]) * (-ey[j]) + ex[i] * ex[j] + 0.0 * 0.0;
+                s[i][j] = s[j][i] = div_by(dot, R);
+            }
+        return area;
+    }
+
     // system.hpp:83-95: contrib_j = area * (f(mid_{j+1}) + f(mid_{j+2})) / 6
     __device__ __forceinline__ double load_col(int j, int32_t t, const FieldDesc& f,
                                                const Recip& R6) const {
@@ -179,6 +197,56 @@ struct ElemCol<3> {
             s[i] = div_by(dot, R);
         }
         return vol;
+    }
+
+    // the whole local matrix at once (element-first path), stiffness_col's
+    // operations; n_i . n_j is symmetric operand for operand (s_ij == s_ji)
+    __device__ __forceinline__ double stiffness_all(double s[4][4], const Recip& R6) const {
+        double n[4][3];
+        normals(n);
+        const double vol = volume(n[3], R6);
+        const Recip R = recip(36.0 * vol);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i <= j; ++i) {
+                const double dot = n[i][0] * n[j][0] + n[i][1] * n[j][1] + n[i][2] * n[j][2];
+                s[i][j] = s[j][i] = div_by(dot, R);
+            }
+        return vol;
+    }
+
+    // load_col for every j at once: the quadrature weights w_q are shared
+    __device__ __forceinline__ void load_all(int32_t t, double vol, const FieldDesc& f,
+                                             double out[4]) const {
+        double w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double fx;
+            if (f.kind == FL_FIELD_SAMPLES) {
+                fx = __ldg(f.samples + (size_t)t * 4 + q);
+            } else if (f.kind == FL_FIELD_CONST) {
+                fx = f.value;
+            } else {
+                double px = 0.0, py = 0.0, pz = 0.0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double lam = (k == q) ? kTet4A : kTet4B;
+                    px += lam * x[k];
+                    py += lam * y[k];
+                    pz += lam * z[k];
+                }
+                fx = eval_point(f, px, py, pz);
+            }
+            w[q] = vol * 0.25 * fx;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += w[q] * ((q == j) ? kTet4A : kTet4B);
+            out[j] = f.kind == FL_FIELD_NONE ? 0.0 : acc;
+        }
     }
 
     // system.hpp:97-111: w_q = vol * 0.25 * f(x_q); contrib_j = sum_q w_q * lambda_qj

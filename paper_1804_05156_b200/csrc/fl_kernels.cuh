@@ -53,6 +53,10 @@ struct ColParams {
     int32_t* tile_off;   // [2][n_tiles + 1]: exclusive scans of tile_tot
     int32_t* colcnt_a;   // [N] in-tile inclusive count after column c
     int32_t* colcnt_f;   // [N] same for A(free, free) (indexed by column c)
+    // element-first records (k_elem_records): one 64-byte record per incidence
+    // (t, j) at srec + (t*(d+1) + j)*8: s_0j..s_dj, load share, the d+1 vertices
+    double* srec;
+    double* lrec;  // unused
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
@@ -70,7 +74,7 @@ int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
 int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
                         double* qi);
 int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
-int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre);
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
 int finish_staging(fl_ctx* ctx, ColParams& p, int tc);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
