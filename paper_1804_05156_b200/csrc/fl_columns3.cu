@@ -8,21 +8,21 @@
 //      incidence in (j, t) order -- the order in which the reference's
 //      blockwise triplets reach column c (assembly.hpp:486-498 after the stable
 //      passes sparse.hpp:79-89);
-//   2. each lane computes its element's column j: s_ij (i = 0..d) and the load
-//      share (fl_geometry.cuh, FMA-free, exact division);
+//   2. each lane reads its incidence's 64-byte element record (k_elem_records:
+//      s_ij for i = 0..d, the load share, the vertices; FMA-free, exact
+//      division) -- or, with FL_KERNEL=3, computes them itself (fl_geometry.cuh);
 //   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
 //      A(c,c) = fold of s_jj in lane order (its items are exactly those): the
 //      shares are staged in smem and group lanes 0 / 1 run the two folds;
-//   4. off-diagonal items (i != j): per pass i, lanes with the same row are found
-//      with match_any; the pass's group leader inserts the row in the group's
-//      small smem hash (CAS), reserves popc(match) positions in the slot's item
-//      list and broadcasts (slot, first position); each item stores itself at
-//      first + rank-in-match.  A slot's list is thus in (i, then lane) order =
-//      the reference's (i*(d+1)+j, t); one lane per slot then folds its list;
+//   4. off-diagonal items (i != j) are staged at itm[i][lane]; per pass i, lanes
+//      with the same row are found with match_any, the group leader inserts the
+//      row in the group's small smem hash (CAS) and stores the pass's lane mask
+//      for that slot; the slot's lane then folds its items pass by pass, lanes
+//      ascending = the reference's (i*(d+1)+j, t) order;
 //   5. slots ranked by row, exact zeros dropped (sparse.hpp:105), A(free,free)
 //      rows kept, all written to the tile staging (k_stage_copy places them).
-// Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, more
-// distinct rows than the group table holds, or more than CAP items on one row.
+// Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, or
+// more distinct rows than the group table holds.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -41,7 +41,6 @@ struct V3 {
     static constexpr int GPW = 32 / L;                 // column groups per warp
     static constexpr int HS = D == 2 ? 16 : 32;        // slot table entries per group
     static constexpr int MAXS = D == 2 ? 12 : 24;      // distinct rows accepted per column
-    static constexpr int CAP = D == 2 ? 8 : 16;        // items per off-diagonal row
     static constexpr int WTC = D == 2 ? 32 : 8;        // columns per warp tile
     static constexpr int ITERS = WTC / GPW;            // group iterations per warp tile
     static constexpr int WARPS = 4;                    // warps per CTA
@@ -50,11 +49,13 @@ struct V3 {
 template <int D, int L>
 struct V3Smem {  // one per group
     alignas(16) int32_t row[V3<D, L>::HS];  // slot -> row (-1 empty)
-    int32_t cnt[V3<D, L>::HS];              // slot -> items listed
-    int32_t srow[V3<D, L>::HS];             // rows in ascending order
+    alignas(16) int32_t crow[V3<D, L>::HS];  // occupied rows, compacted (-1 padded)
+    uint4 msk[V3<D, L>::HS];                 // slot -> per-pass lane mask of its items
+    int32_t srow[V3<D, L>::HS];              // rows in ascending order
     double sval[V3<D, L>::HS];
-    double lb[L], ld[L];                    // load shares / s_jj in lane order
-    double item[V3<D, L>::CAP][V3<D, L>::HS];  // per-slot item lists, position-major
+    alignas(16) double lb[L];                // load shares in lane order
+    alignas(16) double ld[L];                // s_jj in lane order
+    double itm[D + 1][L];                    // item (i, lane) = s_i of the lane's element
 };
 
 __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* nodes, int dim,
@@ -275,27 +276,42 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
             double fold = g == 0 ? 0.0 : -0.0;
             if (g < 2) {
                 const double* src = g == 0 ? sm.lb : sm.ld;
-                for (int q = 0; q < m; ++q) fold = fold + src[q];
+                const double2* src2 = reinterpret_cast<const double2*>(src);
+                int q = 0;
+                for (; q + 1 < m; q += 2) {
+                    const double2 v = src2[q >> 1];
+                    fold = fold + v.x;
+                    fold = fold + v.y;
+                }
+                if (q < m) fold = fold + src[q];
             }
             const double b = __shfl_sync(FULL, fold, 0, L);
             const double dg = __shfl_sync(FULL, fold, 1, L);
-            // ---- 4. off-diagonal items into per-row lists in (i, lane) order
+            // ---- 4. off-diagonal items.  Item (i, lane) sits at itm[i][lane]; per
+            //      pass i the group leader of each row finds the row's slot (CAS
+            //      insert) and records the pass's lane mask msk[slot][i].  Slot h
+            //      then folds its items pass by pass, lanes ascending: the
+            //      reference's (i*(d+1)+j, t) order.
             if (p.want_a) {
                 for (int h = g; h < C::HS; h += L) {
                     sm.row[h] = -1;
-                    sm.cnt[h] = 0;
+                    sm.crow[h] = -1;
+                    sm.msk[h] = make_uint4(0u, 0u, 0u, 0u);
                 }
+#pragma unroll
+                for (int i = 0; i < NV; ++i) sm.itm[i][g] = s[i];
                 __syncwarp();
-                int nslot = 0;
 #pragma unroll
                 for (int i = 0; i < NV; ++i) {
                     const bool has = valid && i != j;
-                    const uint64_t mk = has ? (((uint64_t)gi << 32) | (uint32_t)R[i])
-                                            : ((1ull << 63) | (uint64_t)lane);
-                    const unsigned gm = __match_any_sync(FULL, mk);
-                    const int rank = __popc(gm & lower);
-                    int sb = -1;  // slot | first position << 8
-                    if (has && rank == 0) {
+                    unsigned gm;
+                    if constexpr (L == 32) {  // one group per warp: rows need no group tag
+                        gm = __match_any_sync(FULL, has ? (uint32_t)R[i] : (0x80000000u | lane));
+                    } else {
+                        gm = __match_any_sync(FULL, has ? (((uint64_t)gi << 32) | (uint32_t)R[i])
+                                                        : ((1ull << 63) | (uint64_t)lane));
+                    }
+                    if (has && (gm & lower) == 0) {  // leader of this row in pass i
                         const int32_t r = R[i];
                         uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
                         int slot = -1;
@@ -307,23 +323,12 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                             }
                             h = (h + 1) & (C::HS - 1);
                         }
-                        if (slot >= 0) {
-                            const int f0 = sm.cnt[slot];
-                            sm.cnt[slot] = f0 + __popc(gm);
-                            sb = slot | (f0 << 8);
-                        } else {
-                            bad = true;
-                        }
-                    }
-                    sb = __shfl_sync(FULL, sb, __ffs(gm) - 1);
-                    if (has && sb >= 0) {
-                        const int pos = (sb >> 8) + rank;
-                        if (pos < C::CAP) sm.item[pos][sb & 0xFF] = s[i];
+                        if (slot >= 0) reinterpret_cast<unsigned*>(&sm.msk[slot])[i] = gm >> (gi * L);
                         else bad = true;
                     }
                     __syncwarp();
                 }
-                // ---- 5. fold each row's list (one lane per slot), rank rows, zero drop
+                // ---- 5. the diagonal slot, the folds, rows ranked, zero drop
                 if (g == 0 && act && m > 0) {
                     uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
                     for (int probe = 0; probe < C::HS; ++probe) {
@@ -335,19 +340,35 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                     }
                 }
                 __syncwarp();
-                for (int h = g; h < C::HS; h += L) {
+                // occupied slots, compacted (rank candidates)
+                int nocc = 0;
+#pragma unroll
+                for (int base = 0; base < C::HS; base += L) {
+                    const int32_t r = sm.row[base + g];
+                    const unsigned bal = __ballot_sync(FULL, r >= 0) & gmask;
+                    if (r >= 0) sm.crow[nocc + __popc(bal & lower)] = r;
+                    nocc += __popc(bal);
+                }
+                __syncwarp();
+                const int n4 = (nocc + 3) >> 2;
+#pragma unroll
+                for (int base = 0; base < C::HS; base += L) {
+                    const int h = base + g;
                     const int32_t r = sm.row[h];
                     if (r >= 0) {
                         double acc = dg;
                         if (r != c) {
                             acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
-                            const int n = min(sm.cnt[h], C::CAP);
-                            for (int k = 0; k < n; ++k) acc = acc + sm.item[k][h];
-                        }
-                        int rk = 0;  // rows below r; empty slots (-1) compare as huge
-                        const int4* r4 = reinterpret_cast<const int4*>(sm.row);
+                            const uint4 mk4 = sm.msk[h];
+                            const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
 #pragma unroll
-                        for (int q = 0; q < C::HS / 4; ++q) {
+                            for (int i = 0; i < NV; ++i)
+                                for (unsigned mm = mk[i]; mm; mm &= mm - 1)
+                                    acc = acc + sm.itm[i][__ffs(mm) - 1];
+                        }
+                        int rk = 0;  // rows below r; unused entries (-1) compare as huge
+                        const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
+                        for (int q = 0; q < n4; ++q) {
                             const int4 v = r4[q];
                             rk += ((uint32_t)v.x < (uint32_t)r) + ((uint32_t)v.y < (uint32_t)r) +
                                   ((uint32_t)v.z < (uint32_t)r) + ((uint32_t)v.w < (uint32_t)r);
@@ -358,15 +379,11 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                         }
                     }
                 }
-                int nv = 0;
-                for (int h = g; h < C::HS; h += L) nv += sm.row[h] >= 0;
-#pragma unroll
-                for (int o = L / 2; o > 0; o >>= 1) nv += __shfl_xor_sync(FULL, nv, o, L);
-                if (nv > C::MAXS) {
+                if (nocc > C::MAXS) {
                     bad = true;
-                    nv = 0;
+                    nocc = 0;
                 }
-                nslot = nv;
+                const int nslot = nocc;
                 __syncwarp();
                 const bool col_free = act && p.want_sys && __ldg(p.fidx + c) >= 0;
                 int na = 0, nf = 0;
