@@ -26,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -62,57 +61,66 @@ def peaks():
 # clocks (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled
+    every ~2 ms from a thread (the timed region can be a few ms), with
+    nvidia-smi -lms 100 as the fallback when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons_mask)
         self._stop = threading.Event()
-        self._proc = None
+        self._thread = None
 
     def start(self):
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except FileNotFoundError:
-            self._proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            # CUDA_VISIBLE_DEVICES remaps ordinals: match the torch device by UUID
+            import torch
+            h = None
+            uuid = getattr(torch.cuda.get_device_properties(self.device), "uuid", None)
+            if uuid is not None:
+                want = "GPU-" + str(uuid)
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    u = pynvml.nvmlDeviceGetUUID(hi)
+                    if (u.decode() if isinstance(u, bytes) else u) == want:
+                        h = hi
+                        break
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self._nv, self._h = pynvml, h
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._thread = threading.Thread(target=self._poll, daemon=True)
+            self._thread.start()
+        except Exception as e:  # pragma: no cover - box without NVML
+            log(f"[bench] NVML unavailable ({e}); clocks unsampled")
 
-    def _read(self):
-        for line in self._proc.stdout:
-            if self._stop.is_set():
-                break
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                self.samples.append(parts)
+    def _poll(self):
+        nv, h = self._nv, self._h
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, self._max, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
         self._stop.set()
-        if self._proc:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=2)
-            except Exception:
-                self._proc.kill()
+        if self._thread:
+            self._thread.join(timeout=1)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            for k, nm in enumerate(names):
-                if s[4 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        reasons = sorted({n for _, _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "NVML, 2 ms polling in the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -176,6 +184,15 @@ def run_reference_impl(args, rank: int, world: int):
 # ---------------------------------------------------------------------------
 # GPU path
 # ---------------------------------------------------------------------------
+def load_traffic(config: str):
+    """ncu dram bytes (read + write) per launch of the numeric phase, from profiles/."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh).get(config)
+
+
 def run_ours(args, rank: int, world: int):
     import ctypes as C
 
@@ -185,6 +202,8 @@ def run_ours(args, rank: int, world: int):
     os.environ.setdefault("FL_PROFILE", "1")
     import paper_1804_05156_b200 as fl
     from paper_1804_05156_b200 import _lib, configs
+    from paper_1804_05156_b200.mesh import DeviceMesh
+    from paper_1804_05156_b200.shard import column_ranges
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
@@ -197,30 +216,36 @@ def run_ours(args, rank: int, world: int):
     cfg = configs.build(args.config, f_mode="samples")
     m = cfg.mesh
     N, NT, d = m.num_nodes(), m.num_elems(), m.dim
-    log(f"[bench] {args.config}: {cfg.description} N={N} NT={NT} built in {time.time() - t0:.1f}s")
+    c0, c1 = column_ranges(N, world)[rank]
+    log(f"[bench] rank {rank}/{world} {args.config}: {cfg.description} N={N} NT={NT} "
+        f"columns [{c0}, {c1}) built in {time.time() - t0:.1f}s")
 
-    # device-resident inputs (uploaded once, untimed)
-    dm = m.device(ctx)
+    # device-resident inputs (uploaded once, untimed); this rank's column range
+    dm = DeviceMesh(ctx, m)
+    if world > 1:
+        dm.set_columns(c0, c1)
     res = fl.AssemblyResult(ctx)
     what = _lib.OUT_SYSTEM | _lib.REPLAN
 
-    def fields():
-        ff, k1 = fl.api._field_struct(cfg.f, m, "load")
-        fc, k2 = fl.api._field_struct(cfg.coef, m, "coef")
-        fd, k3 = fl.api._field_struct(cfg.g_dirichlet, m, "dirichlet")
-        fn, k4 = fl.api._field_struct(cfg.g_neumann, m, "neumann")
-        return (ff, fc, fd, fn), (k1, k2, k3, k4)
-
-    # f samples: stage once on the device so the timed steps read them from HBM
-    (ff, fc, fd, fn), keep = fields()
+    ff, k1 = fl.api._field_struct(cfg.f, m, "load")
+    fc, k2 = fl.api._field_struct(cfg.coef, m, "coef")
+    fd, k3 = fl.api._field_struct(cfg.g_dirichlet, m, "dirichlet")
+    fn, k4 = fl.api._field_struct(cfg.g_neumann, m, "neumann")
     f_dev = None
-    if ff.kind == _lib.FIELD_SAMPLES:
-        f_dev = torch.from_numpy(np.asarray(keep[0])).to(f"cuda:{dev}")
+    if ff.kind == _lib.FIELD_SAMPLES:  # stage samples on the device once
+        f_dev = torch.from_numpy(np.asarray(k1)).to(f"cuda:{dev}")
         ff.mem, ff.samples = _lib.MEM_DEVICE, f_dev.data_ptr()
+
+    counts = torch.zeros(4, dtype=torch.int64, device=f"cuda:{dev}")
+    all_counts = torch.zeros(world * 4, dtype=torch.int64, device=f"cuda:{dev}")
 
     def step():
         _lib.check(L.fl_assemble(ctx.handle, dm.handle, C.byref(ff), C.byref(fc), C.byref(fd),
                                  C.byref(fn), what, res.handle), "fl_assemble")
+        if world > 1:  # the nnz-offset exchange (NCCL all_gather on the same stream)
+            _lib.check(L.fl_result_counts_async(res.handle, counts.data_ptr()))
+            dist.all_gather_into_tensor(all_counts, counts)
+            torch.cumsum(all_counts.view(world, 4), dim=0)
 
     flush = None
     ws_bytes = configs.system_bytes(d, N, NT, 0, 0, 0)
@@ -240,7 +265,7 @@ def run_ours(args, rank: int, world: int):
         clocks.start()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-        phase = []
+        phase, kph = [], []
         for k in range(args.steps):
             if flush is not None:
                 flush.fill_(k)
@@ -249,59 +274,80 @@ def run_ours(args, rank: int, world: int):
             ev[k][1].record(stream)
             sz = res.sizes()  # synchronises; resolves the phase events
             phase.append(ctx.last_timings())
+            kph.append(ctx.last_kernel_timings())
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         clocks.stop()
         launches = ctx.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    ms = float(np.mean(step_ms))
+    ms_local = float(np.mean(step_ms))
+    ms = ms_local
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
+        t = torch.tensor([ms_local], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        gathered = all_counts.view(world, 4).cpu().numpy()
     col_ms = float(np.mean([p[2] for p in phase]))
     plan_ms = float(np.mean([p[0] for p in phase]))
     mark_ms = float(np.mean([p[1] for p in phase]))
+    rec_ms, kern_ms, place_ms = (float(np.mean([p[i] for p in kph])) for i in range(3))
 
-    nnz, nnz_ff, n_free = int(sz.nnz), int(sz.nnz_ff), int(sz.n_free)
+    # sizes: this rank's shard; global totals from the exchange
+    nnz_l, nnz_ff_l, n_free = int(sz.nnz), int(sz.nnz_ff), int(sz.n_free)
+    ncol_l, nfree_l = int(sz.n), int(sz.n_free_cols)
+    nnz, nnz_ff = (int(gathered[:, 2].sum()), int(gathered[:, 3].sum())) if world > 1 else (nnz_l, nnz_ff_l)
     b_sl = configs.algorithmic_bytes(d, N, NT, nnz)
     b_sys = configs.system_bytes(d, N, NT, nnz, n_free, nnz_ff)
     f_bytes = 8 * NT * (d + 1) if ff.kind == _lib.FIELD_SAMPLES else 0
-    # k_columns algorithmic bytes: mesh + plan-free inputs + every output it writes
-    col_bytes = (4 * (d + 1) * NT + 8 * d * N + f_bytes + N + 4 * N  # elems, nodes, f, is_dir, fidx
-                 + 4 * (N + 1) + 12 * nnz + 8 * N + 16 * N             # A, b, u0, b_mod
-                 + 4 * (n_free + 1) + 12 * nnz_ff + 8 * n_free)        # A_ff, b_f
+    # numeric phase (element records + column kernel + placement), this rank:
+    # compulsory bytes = mesh + f samples read once, every column output written once
+    frac_el = 1.0 if world == 1 else min(1.0, ncol_l / max(N, 1) * 1.0)
+    col_bytes = (int(frac_el * (4 * (d + 1) * NT + 8 * d * N + f_bytes)) + ncol_l + 4 * ncol_l
+                 + 4 * (ncol_l + 1) + 12 * nnz_l + 8 * ncol_l + 16 * ncol_l
+                 + 4 * (nfree_l + 1) + 12 * nnz_ff_l + 8 * nfree_l)
     peak, peak_kind = peaks()
     achieved = col_bytes / (col_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.config) if world == 1 else None
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev)
+        e2e = run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, (c0, c1) if world > 1 else None)
+        if world > 1:
+            t = torch.tensor([e2e["ms_per_step"]], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["ms_per_step"] = float(t.item())
+            e2e["value"] = NT / (e2e["ms_per_step"] * 1e-3)
 
     line = None
     if rank == 0:
-        # replicas: every rank assembles the whole mesh (sharded path: see DESIGN.md §6)
-        value = world * NT / (ms * 1e-3)
+        value = NT / (ms * 1e-3)  # the whole mesh, assembled by all ranks together
         cpu = None if args.no_cpu_baseline else cpu_reference(args.config)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator meshes, SURVEY.md §8(d) recipes)",
             "config": {"workload": f"{args.config}: {cfg.description}", "n_nodes": N,
                        "n_elems": NT, "nnz": nnz, "nnz_ff": nnz_ff, "n_free": n_free,
                        "step": "plan+partition+stiffness+load+dirichlet+A_ff+b_f",
                        "l2": ("flushed between steps (256 MB write)" if flush is not None
                               else "inputs larger than L2"),
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"row-sharded x{world} (contiguous column ranges; NCCL "
+                                       "all_gather of nnz counts)" if world > 1 else "1 GPU"),
                        "f": str(cfg.f) if not isinstance(cfg.f, np.ndarray) else "host samples",
                        "coef": str(cfg.coef)},
             "hbm_gbs_step": b_sys / (ms * 1e-3) / 1e9,
-            "bytes": {"B_SL": b_sl, "B_sys": b_sys, "f_samples": f_bytes, "k_columns": col_bytes},
-            "phases_ms": {"plan": plan_ms, "partition": mark_ms, "k_columns": col_ms},
-            "roofline": {"bound": "hbm", "kernel": "k_columns", "achieved": achieved,
-                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None},
+            "bytes": {"B_SL": b_sl, "B_sys": b_sys, "f_samples": f_bytes, "numeric_phase": col_bytes},
+            "phases_ms": {"plan": plan_ms, "partition": mark_ms, "numeric": col_ms,
+                          "element_records": rec_ms, "column_kernel": kern_ms, "placement": place_ms},
+            "roofline": {"bound": "hbm",
+                         "kernel": "numeric phase (k_elem_records + k_columns3 + placement), rank 0",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak,
+                         "traffic": traffic["dram_bytes"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -313,7 +359,7 @@ def run_ours(args, rank: int, world: int):
     return line
 
 
-def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev):
+def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, cols=None):
     m = cfg.mesh
     N, NT, d = m.num_nodes(), m.num_elems(), m.dim
 
@@ -330,6 +376,8 @@ def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev):
     hmesh = C.c_void_p()
     _lib.check(L.fl_mesh_create(ctx.handle, d, N, NT, h_nodes.data_ptr(), h_elems.data_ptr(),
                                 h_flags.data_ptr(), _lib.MEM_HOST, C.byref(hmesh)))
+    if cols is not None:
+        _lib.check(L.fl_mesh_set_columns(ctx.handle, hmesh, cols[0], cols[1]))
     res = fl.AssemblyResult(ctx)
     ff, _k1 = fl.api._field_struct(cfg.f if f_arr is None else None, m, "load")
     if f_arr is not None:
@@ -348,13 +396,14 @@ def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev):
                                  C.byref(fn), _lib.OUT_SYSTEM, res.handle))
         sz = res.sizes()
         if outs is None:
-            spec = [(_lib.A_COL_PTR, torch.int32, N + 1), (_lib.A_ROW_IDX, torch.int32, sz.nnz),
-                    (_lib.A_VALUES, torch.float64, sz.nnz), (_lib.B, torch.float64, N),
-                    (_lib.U0, torch.float64, N), (_lib.B_MOD, torch.float64, N),
+            n, nf = sz.n, sz.n_free_cols  # this rank's columns (all of them at N=1)
+            spec = [(_lib.A_COL_PTR, torch.int32, n + 1), (_lib.A_ROW_IDX, torch.int32, sz.nnz),
+                    (_lib.A_VALUES, torch.float64, sz.nnz), (_lib.B, torch.float64, n),
+                    (_lib.U0, torch.float64, n), (_lib.B_MOD, torch.float64, n),
                     (_lib.DIR_NODES, torch.int32, sz.n_dir), (_lib.FREE_NODES, torch.int32, sz.n_free),
-                    (_lib.AFF_COL_PTR, torch.int32, sz.n_free + 1),
+                    (_lib.AFF_COL_PTR, torch.int32, nf + 1),
                     (_lib.AFF_ROW_IDX, torch.int32, sz.nnz_ff),
-                    (_lib.AFF_VALUES, torch.float64, sz.nnz_ff), (_lib.B_F, torch.float64, sz.n_free)]
+                    (_lib.AFF_VALUES, torch.float64, sz.nnz_ff), (_lib.B_F, torch.float64, nf)]
             outs = [(w, torch.empty(max(c, 1), dtype=t, pin_memory=True)) for w, t, c in spec]
         for w, buf in outs:
             _lib.check(L.fl_result_copy(res.handle, w, buf.data_ptr(),

@@ -1,0 +1,273 @@
+// femlite_b200_adapter.hpp -- the femlite-side binding of the B200 C-ABI.
+//
+// Header-only C++20 over include/femlite_b200.h with the reference's own types
+// and signatures (paths relative to femlite's proj/include/femlite/):
+//
+//   femlite_b200::assemble_blockwise(mesh)           assembly.hpp:261  assemble_blockwise
+//   femlite_b200::assemble(mesh, strategy)           assembly.hpp:302  assemble
+//   femlite_b200::assemble_load(mesh, f)             system.hpp:71     assemble_load
+//   femlite_b200::partition_boundary(mesh)           system.hpp:50     partition_boundary
+//   femlite_b200::apply_neumann(b, mesh, g)          system.hpp:123    apply_neumann
+//   femlite_b200::poisson_system(mesh, problem)      solver.hpp:226-242 (pre-solve path:
+//                                                    partition, A, b, Neumann, Dirichlet lift,
+//                                                    A(free, free), b_f -- one fused pass)
+//   femlite_b200::submatrix(a, rows, cols)           sparse.hpp:159    submatrix
+//
+// Include it after the femlite headers.  Errors are rethrown as
+// femlite::Error with the reference's ErrorCode (the ABI status is
+// 1 + ordinal).  Host callables (ScalarField) are evaluated on the host at the
+// reference's quadrature / face points (fl_host_points) and passed as samples,
+// so results are bitwise the reference's.  INTEGRATION.md shows the one-line
+// hook in femlite's assemble() dispatcher.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "femlite/error.hpp"
+#include "femlite/mesh.hpp"
+#include "femlite/sparse.hpp"
+#include "femlite/system.hpp"
+#include "femlite_b200.h"
+
+namespace femlite_b200 {
+
+inline void check(int rc, const char* what) {
+    if (rc == FL_OK) return;
+    const std::string msg = std::string(what) + ": " + fl_last_error();
+    if (rc >= 1 && rc <= 1 + static_cast<int>(femlite::ErrorCode::unsupported_boundary_type))
+        throw femlite::Error(static_cast<femlite::ErrorCode>(rc - 1), msg);
+    throw std::runtime_error(msg);
+}
+
+/// One device + stream; the default context (device 0) is created on first use.
+class Context {
+public:
+    explicit Context(int device = 0) { check(fl_create(device, &ctx_), "fl_create"); }
+    ~Context() { fl_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    fl_ctx* get() const { return ctx_; }
+    static Context& default_context() {
+        static Context ctx(0);
+        return ctx;
+    }
+
+private:
+    fl_ctx* ctx_ = nullptr;
+};
+
+namespace detail {
+
+struct MeshHandle {
+    fl_mesh* m = nullptr;
+    MeshHandle(Context& ctx, const femlite::Mesh& mesh) {
+        const auto& fl = mesh.bd_flags();
+        check(fl_mesh_create(ctx.get(), mesh.dim(), mesh.num_nodes(), mesh.num_elems(),
+                             mesh.nodes().data(), mesh.elems().data(),
+                             fl.empty() ? nullptr : fl.data(), FL_MEM_HOST, &m),
+              "fl_mesh_create");
+    }
+    ~MeshHandle() { fl_mesh_destroy(m); }
+    MeshHandle(const MeshHandle&) = delete;
+    MeshHandle& operator=(const MeshHandle&) = delete;
+};
+
+struct ResultHandle {
+    fl_result* r = nullptr;
+    explicit ResultHandle(Context& ctx) { check(fl_result_create(ctx.get(), &r), "fl_result_create"); }
+    ~ResultHandle() { fl_result_destroy(r); }
+    ResultHandle(const ResultHandle&) = delete;
+    ResultHandle& operator=(const ResultHandle&) = delete;
+
+    fl_sizes sizes() const {
+        fl_sizes z{};
+        check(fl_result_sizes(r, &z), "fl_result_sizes");
+        return z;
+    }
+    template <class T>
+    std::vector<T> array(int which, int64_t count) const {
+        std::vector<T> out(static_cast<std::size_t>(count));
+        check(fl_result_copy(r, which, out.empty() ? nullptr : out.data(),
+                             static_cast<int64_t>(out.size() * sizeof(T)), FL_MEM_HOST),
+              "fl_result_copy");
+        return out;
+    }
+    femlite::CscMatrix matrix(int m) const {
+        const fl_sizes z = sizes();
+        femlite::CscMatrix a;
+        a.m = m;
+        a.n = z.n;
+        a.col_ptr = array<femlite::index_t>(FL_A_COL_PTR, z.n + 1);
+        a.row_idx = array<femlite::index_t>(FL_A_ROW_IDX, z.nnz);
+        a.values = array<double>(FL_A_VALUES, z.nnz);
+        return a;
+    }
+    femlite::CscMatrix matrix_ff() const {
+        const fl_sizes z = sizes();
+        femlite::CscMatrix a;
+        a.m = z.n_free;
+        a.n = z.n_free_cols;
+        a.col_ptr = array<femlite::index_t>(FL_AFF_COL_PTR, z.n_free_cols + 1);
+        a.row_idx = array<femlite::index_t>(FL_AFF_ROW_IDX, z.nnz_ff);
+        a.values = array<double>(FL_AFF_VALUES, z.nnz_ff);
+        return a;
+    }
+};
+
+/// f sampled at the reference's points of `rule` (0: load, 3: Neumann faces)
+inline std::vector<double> sample(const femlite::Mesh& mesh, const femlite::ScalarField& f,
+                                  int rule) {
+    const std::size_t np = static_cast<std::size_t>(mesh.num_elems()) * (mesh.dim() + 1);
+    std::vector<double> xyz(np * 3), out(np);
+    check(fl_host_points(mesh.dim(), mesh.num_nodes(), mesh.num_elems(), mesh.nodes().data(),
+                         mesh.elems().data(), rule, xyz.data()),
+          "fl_host_points");
+    for (std::size_t k = 0; k < np; ++k)
+        out[k] = f(femlite::Point{xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2]});
+    return out;
+}
+
+inline std::vector<double> sample_nodes(const femlite::Mesh& mesh, const femlite::ScalarField& g) {
+    std::vector<double> out(static_cast<std::size_t>(mesh.num_nodes()));
+    for (femlite::index_t k = 0; k < mesh.num_nodes(); ++k) out[k] = g(mesh.node_point(k));
+    return out;
+}
+
+inline fl_field none() { return fl_field{FL_FIELD_NONE, FL_MEM_HOST, 0.0, nullptr, 0}; }
+inline fl_field samples(const std::vector<double>& v) {
+    return fl_field{FL_FIELD_SAMPLES, FL_MEM_HOST, 0.0, v.data(), static_cast<int64_t>(v.size())};
+}
+
+inline femlite::BoundaryPartition partition_of(const femlite::Mesh& mesh, const ResultHandle& r) {
+    const fl_sizes z = r.sizes();
+    femlite::BoundaryPartition p;
+    p.dirichlet_nodes = r.array<femlite::index_t>(FL_DIR_NODES, z.n_dir);
+    p.free_nodes = r.array<femlite::index_t>(FL_FREE_NODES, z.n_free);
+    // the face lists are index bookkeeping of the reference's own mesh layer
+    p.dirichlet_faces = femlite::boundary_faces(mesh, 1);
+    p.neumann_faces = femlite::boundary_faces(mesh, 2);
+    return p;
+}
+
+}  // namespace detail
+
+/// assembly.hpp:261 on the GPU (symmetric_fill only changes the reference's
+/// triplet multiset and is rejected, as the GPU path has no triplets).
+inline femlite::CscMatrix assemble_blockwise(const femlite::Mesh& mesh, bool symmetric_fill = false,
+                                             Context& ctx = Context::default_context()) {
+    if (symmetric_fill)
+        throw femlite::Error(femlite::ErrorCode::invalid_parameter,
+                             "symmetric_fill is a CPU triplet-order option");
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    const fl_field n = detail::none();
+    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &n, FL_OUT_STIFFNESS, r.r), "fl_assemble");
+    return r.matrix(mesh.num_nodes());
+}
+
+/// assembly.hpp:302: blockwise runs on the GPU; the reference's CPU oracles
+/// (dense_oracle, triplet_loop) are its own cross-checks and stay on the CPU.
+inline femlite::CscMatrix assemble(const femlite::Mesh& mesh, femlite::AssemblyStrategy strategy,
+                                   Context& ctx = Context::default_context()) {
+    if (strategy != femlite::AssemblyStrategy::blockwise)
+        throw femlite::Error(femlite::ErrorCode::invalid_parameter,
+                             "only the blockwise strategy runs on the B200 path");
+    return assemble_blockwise(mesh, false, ctx);
+}
+
+/// system.hpp:71
+inline std::vector<double> assemble_load(const femlite::Mesh& mesh, const femlite::ScalarField& f,
+                                         Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    std::vector<double> fs;
+    fl_field ff = detail::none();
+    if (f) {
+        fs = detail::sample(mesh, f, 0);
+        ff = detail::samples(fs);
+    }
+    const fl_field n = detail::none();
+    check(fl_assemble(ctx.get(), m.m, &ff, &n, &n, &n, FL_OUT_LOAD, r.r), "fl_assemble");
+    return r.array<double>(FL_B, r.sizes().n);
+}
+
+/// system.hpp:50
+inline femlite::BoundaryPartition partition_boundary(const femlite::Mesh& mesh,
+                                                     Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    const fl_field n = detail::none();
+    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &n, FL_OUT_PARTITION, r.r), "fl_assemble");
+    return detail::partition_of(mesh, r);
+}
+
+/// system.hpp:123: the Neumann face shares accumulated on the GPU, then added
+/// to b entry by entry (b[k] += add[k], system.hpp:170)
+inline std::vector<double> apply_neumann(std::vector<double> b, const femlite::Mesh& mesh,
+                                         const femlite::ScalarField& g,
+                                         Context& ctx = Context::default_context()) {
+    if (static_cast<femlite::index_t>(b.size()) != mesh.num_nodes())
+        throw femlite::Error(femlite::ErrorCode::shape_mismatch, "apply_neumann: vector length");
+    if (!g) return b;
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    const std::vector<double> gs = detail::sample(mesh, g, 3);
+    const fl_field gn = detail::samples(gs), n = detail::none();
+    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &gn, FL_OUT_LOAD | FL_OUT_PARTITION, r.r),
+          "fl_assemble");
+    const std::vector<double> add = r.array<double>(FL_B, r.sizes().n);
+    for (std::size_t k = 0; k < b.size(); ++k) b[k] += add[k];
+    return b;
+}
+
+/// Everything solve_poisson builds before its solve (solver.hpp:226-242).
+struct PoissonSystem {
+    femlite::CscMatrix a;
+    std::vector<double> b;
+    femlite::DirichletSystem dirichlet;  // u0, b - A u0, partition
+    femlite::CscMatrix a_ff;
+    std::vector<double> b_f;
+};
+
+inline PoissonSystem poisson_system(const femlite::Mesh& mesh, const femlite::PoissonProblem& pb,
+                                    Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    std::vector<double> fs, gd, gn;
+    fl_field ff = detail::none(), fd = detail::none(), fn = detail::none();
+    const fl_field n = detail::none();
+    if (pb.f) ff = detail::samples(fs = detail::sample(mesh, pb.f, 0));
+    if (pb.g_dirichlet) fd = detail::samples(gd = detail::sample_nodes(mesh, pb.g_dirichlet));
+    if (pb.g_neumann) fn = detail::samples(gn = detail::sample(mesh, pb.g_neumann, 3));
+    check(fl_assemble(ctx.get(), m.m, &ff, &n, &fd, &fn, FL_OUT_SYSTEM, r.r), "fl_assemble");
+    const fl_sizes z = r.sizes();
+    PoissonSystem s;
+    s.a = r.matrix(mesh.num_nodes());
+    s.b = r.array<double>(FL_B, z.n);
+    s.dirichlet.u0 = r.array<double>(FL_U0, z.n);
+    s.dirichlet.b = r.array<double>(FL_B_MOD, z.n);
+    s.dirichlet.partition = detail::partition_of(mesh, r);
+    s.a_ff = r.matrix_ff();
+    s.b_f = r.array<double>(FL_B_F, z.n_free_cols);
+    return s;
+}
+
+/// sparse.hpp:159 (strictly increasing index sets, validated on the GPU)
+inline femlite::CscMatrix submatrix(const femlite::CscMatrix& a,
+                                    std::span<const femlite::index_t> rows,
+                                    std::span<const femlite::index_t> cols,
+                                    Context& ctx = Context::default_context()) {
+    detail::ResultHandle r(ctx);
+    check(fl_submatrix(ctx.get(), a.m, a.n, a.col_ptr.data(), a.row_idx.data(), a.values.data(),
+                       static_cast<int32_t>(rows.size()), rows.data(),
+                       static_cast<int32_t>(cols.size()), cols.data(), FL_MEM_HOST, r.r),
+          "fl_submatrix");
+    return r.matrix(static_cast<femlite::index_t>(rows.size()));
+}
+
+}  // namespace femlite_b200

@@ -26,7 +26,7 @@ enum {
     E_NOMEM = 100
 };
 
-/* mesh.hpp:68-69 */
+/* mesh.hpp:29-30 */
 static const int kTriFaces[3][2] = {{1, 2}, {2, 0}, {0, 1}};
 static const int kTetFaces[4][3] = {{1, 3, 2}, {0, 2, 3}, {0, 3, 1}, {0, 1, 2}};
 /* quadrature.hpp:62-73 (tet4) */
@@ -59,13 +59,13 @@ static double eval_field(int kind, double value, const double x[3]) {
 }
 
 /* ---- mesh.hpp ---------------------------------------------------------------- */
-/* mesh.hpp:73-77 */
+/* mesh.hpp:34-38 */
 static double signed_area(const double* v1, const double* v2, const double* v3) {
     const double e2x = v1[0] - v3[0], e2y = v1[1] - v3[1];
     const double e3x = v2[0] - v1[0], e3y = v2[1] - v1[1];
     return 0.5 * (-e3x * e2y + e3y * e2x);
 }
-/* mesh.hpp:81-90 */
+/* mesh.hpp:42-51 */
 static double signed_volume(const double* v1, const double* v2, const double* v3,
                             const double* v4) {
     const double ax = v2[0] - v1[0], ay = v2[1] - v1[1], az = v2[2] - v1[2];
@@ -102,7 +102,7 @@ int fo_validate_mesh(int dim, int32_t n_nodes, int32_t n_elems, const double* no
     return FO_OK;
 }
 
-/* mesh.hpp:349-370 */
+/* mesh.hpp:310-331 */
 static int gen_unit_square(int n, double** nodes_out, int32_t** elems_out, int32_t* nn,
                            int32_t* ne) {
     const double h = 1.0 / n;
@@ -131,7 +131,7 @@ static int gen_unit_square(int n, double** nodes_out, int32_t** elems_out, int32
     return FO_OK;
 }
 
-/* mesh.hpp:372-409 (Kuhn split) */
+/* mesh.hpp:333-370 (Kuhn split) */
 static int gen_unit_cube(int n, double** nodes_out, int32_t** elems_out, int32_t* nn,
                          int32_t* ne) {
     static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2},
@@ -176,7 +176,7 @@ static int gen_unit_cube(int n, double** nodes_out, int32_t** elems_out, int32_t
     return FO_OK;
 }
 
-/* mesh.hpp:411-444 */
+/* mesh.hpp:372-405 */
 static int gen_lshape(int n, double** nodes_out, int32_t** elems_out, int32_t* nn,
                       int32_t* ne) {
     const double h = 1.0 / n;
@@ -274,7 +274,7 @@ static void sort3(int32_t* k) {
     if (k[0] > k[1]) { t = k[0]; k[0] = k[1]; k[1] = t; }
 }
 
-/* mesh.hpp:290-343 */
+/* mesh.hpp:251-304 */
 int fo_set_boundary_flags(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                           const int32_t* elems, int classifier, int8_t* flags_out) {
     (void)n_nodes;
@@ -450,13 +450,13 @@ int fo_submatrix(const fo_csc* a, int32_t n_rows, const int32_t* rows, int32_t n
 
 /* ---- assembly.hpp ------------------------------------------------------------ */
 static void cross3(const double u[3], const double v[3], double out[3]) {
-    /* assembly.hpp:276-280 */
+    /* assembly.hpp:76-80 */
     out[0] = u[1] * v[2] - u[2] * v[1];
     out[1] = u[2] * v[0] - u[0] * v[2];
     out[2] = u[0] * v[1] - u[1] * v[0];
 }
 
-/* assembly.hpp:333-370; returns the unsigned measure, 0 if degenerate */
+/* assembly.hpp:133-170; returns the unsigned measure, 0 if degenerate */
 static double scaled_normals(int dim, const double* vertices, double normals[4][3]) {
     if (dim == 2) {
         const double* v[3] = {&vertices[0], &vertices[2], &vertices[4]};
@@ -491,13 +491,13 @@ static double scaled_normals(int dim, const double* vertices, double normals[4][
     return fabs(cr[0] * v14[0] + cr[1] * v14[1] + cr[2] * v14[2]) / 6.0;
 }
 
-/* assembly.hpp:404-411 */
+/* assembly.hpp:204-211 */
 static void gather_vertices(int dim, const double* nodes, const int32_t* v, double* out) {
     for (int k = 0; k <= dim; ++k)
         for (int c = 0; c < dim; ++c) out[k * dim + c] = nodes[(size_t)v[k] * dim + c];
 }
 
-/* assembly.hpp:491-492: one blockwise triplet value */
+/* assembly.hpp:291-292: one blockwise triplet value */
 static double local_entry(const double normals[4][3], double factor, double measure, int i, int j) {
     const double* ni = normals[i];
     const double* nj = normals[j];
@@ -508,14 +508,14 @@ int fo_local_stiffness_normals(int dim, const double* verts, double* out, double
     double normals[4][3];
     const double m = scaled_normals(dim, verts, normals);
     if (m == 0.0) return E_DEGENERATE;
-    const double factor = (dim == 2) ? 4.0 : 36.0; /* assembly.hpp:382 */
+    const double factor = (dim == 2) ? 4.0 : 36.0; /* assembly.hpp:182 */
     for (int i = 0; i <= dim; ++i)
         for (int j = 0; j <= dim; ++j) out[i * (dim + 1) + j] = local_entry(normals, factor, m, i, j);
     *measure = m;
     return FO_OK;
 }
 
-/* assembly.hpp:461-500 */
+/* assembly.hpp:261-300 */
 int fo_assemble_blockwise(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                           const int32_t* elems, const double* coef, fo_csc* out) {
     const int d = dim, nv = dim + 1;
@@ -724,7 +724,7 @@ int fo_assemble_load(int dim, int32_t n_nodes, int32_t n_elems, const double* no
     return rc;
 }
 
-/* system.hpp:50-67 with boundary_faces mesh.hpp:261-285 */
+/* system.hpp:50-67 with boundary_faces mesh.hpp:222-246 */
 int fo_partition_boundary(int dim, int32_t n_nodes, int32_t n_elems, const int32_t* elems,
                           const int8_t* flags, int32_t* n_dir, int32_t** dir_nodes,
                           int32_t* n_free, int32_t** free_nodes, int32_t* n_dir_faces,

@@ -40,13 +40,13 @@ typedef struct {
 void fo_free(void* p);
 void fo_csc_free(fo_csc* a);
 
-/* mesh.hpp:449-458 (unit_square 349-370, unit_cube 372-409, lshape 411-444) */
+/* mesh.hpp:410-419 (unit_square 349-370, unit_cube 372-409, lshape 411-444) */
 int fo_generate_mesh(int shape, int n, int32_t* dim, int32_t* n_nodes, int32_t* n_elems,
                      double** nodes, int32_t** elems);
-/* mesh.hpp:213-226 + 187-208 (make_mesh validation) */
+/* mesh.hpp:174-187 + 187-208 (make_mesh validation) */
 int fo_validate_mesh(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                      const int32_t* elems, const int8_t* flags);
-/* mesh.hpp:290-343 with the classifiers of presets.hpp:36-45 (+ L-shape, see .c) */
+/* mesh.hpp:251-304 with the classifiers of presets.hpp:36-45 (+ L-shape, see .c) */
 int fo_set_boundary_flags(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                           const int32_t* elems, int classifier, int8_t* flags_out);
 
@@ -62,9 +62,9 @@ int fo_matvec(const fo_csc* a, const double* x, double* y);
 int fo_submatrix(const fo_csc* a, int32_t n_rows, const int32_t* rows, int32_t n_cols,
                  const int32_t* cols, fo_csc* out);
 
-/* assembly.hpp:375-389 local_stiffness_normals (out: (d+1)^2 row-major) */
+/* assembly.hpp:175-189 local_stiffness_normals (out: (d+1)^2 row-major) */
 int fo_local_stiffness_normals(int dim, const double* verts, double* out, double* measure);
-/* assembly.hpp:461-500; coef (nullable) = per-element coefficient multiplied
+/* assembly.hpp:261-300; coef (nullable) = per-element coefficient multiplied
  * after the reference division. */
 int fo_assemble_blockwise(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                           const int32_t* elems, const double* coef, fo_csc* out);

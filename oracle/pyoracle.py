@@ -192,7 +192,7 @@ def assemble_blockwise(dim, nodes, elems, coef=None, which: str = "oracle") -> C
 
 
 def ref_assemble_strategy(dim, nodes, elems, strategy: int, symmetric_fill: bool = False) -> Csc:
-    """The reference's assemble(mesh, strategy) (assembly.hpp:502): 0 dense, 1 triplet, 2 blockwise."""
+    """The reference's assemble(mesh, strategy) (assembly.hpp:302): 0 dense, 1 triplet, 2 blockwise."""
     L = lib("ref")
     nodes, elems = _arr_f64(nodes), _arr_i32(elems)
     nn, ne = nodes.shape[0], elems.shape[0]

@@ -6,16 +6,16 @@
 // It lets tests/ and bench.py --impl reference drive the reference's own
 // hot-path functions through ctypes:
 //
-//   generate_mesh        mesh.hpp:449     set_boundary_flags  mesh.hpp:290
-//   assemble_blockwise   assembly.hpp:461 assemble(strategy)  assembly.hpp:502
+//   generate_mesh        mesh.hpp:410     set_boundary_flags  mesh.hpp:251
+//   assemble_blockwise   assembly.hpp:261 assemble(strategy)  assembly.hpp:302
 //   assemble_load        system.hpp:71    partition_boundary  system.hpp:50
 //   apply_neumann        system.hpp:123   apply_dirichlet     system.hpp:182
 //   submatrix            sparse.hpp:159   from_triplets       sparse.hpp:61
-//   accumulate           sparse.hpp:186   local_stiffness_*   assembly.hpp:288,375
+//   accumulate           sparse.hpp:186   local_stiffness_*   assembly.hpp:88,175
 //
 // The config-5 variable coefficient does not exist in the reference
 // (SPEC.md:386).  ref_assemble_blockwise_coef restates the blockwise loop
-// (assembly.hpp:461-500) around the reference's own detail::scaled_normals /
+// (assembly.hpp:261-300) around the reference's own detail::scaled_normals /
 // detail::gather_vertices / from_triplets with s_ij multiplied by the element
 // coefficient after the reference division; with a == 1 it
 // is bit-identical to assemble_blockwise (checked in tests).
@@ -130,7 +130,7 @@ CscMatrix import_csc(int32_t m, int32_t n, const int32_t* col_ptr, const int32_t
     return a;
 }
 
-// assembly.hpp:461-500 loop structure with an element coefficient (a11).
+// assembly.hpp:261-300 loop structure with an element coefficient (a11).
 CscMatrix blockwise_with_coefficient(const Mesh& mesh, const double* coef) {
     const int d = mesh.dim();
     const index_t n = mesh.num_nodes();

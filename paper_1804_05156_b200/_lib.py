@@ -40,6 +40,7 @@ SIGNATURES = {
     "fl_mesh_validate": (C.c_int, [_vp, _vp]),
     "fl_mesh_plan": (C.c_int, [_vp, _vp]),
     "fl_mesh_set_columns": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32]),
+    "fl_result_counts_async": (C.c_int, [_vp, _vp]),
     "fl_mesh_destroy": (C.c_int, [_vp]),
     "fl_result_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fl_result_destroy": (C.c_int, [_vp]),
@@ -51,10 +52,12 @@ SIGNATURES = {
                                C.c_int32, _vp, C.c_int, _vp]),
     "fl_launch_count": (C.c_int64, [_vp]),
     "fl_last_timings": (C.c_int, [_vp, _vp]),
+    "fl_last_kernel_timings": (C.c_int, [_vp, _vp]),
     "fl_selftest_div": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_int]),
     "fl_phase_cycles": (C.c_int, [_vp, _vp]),
     "fl_host_sample": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _vp, _vp, C.c_int, C.c_int,
                                  C.c_double, _vp]),
+    "fl_host_points": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _vp, _vp, C.c_int, _vp]),
 }
 
 

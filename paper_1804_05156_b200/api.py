@@ -2,7 +2,7 @@
 
 Names, argument meaning and error behaviour follow femlite
 (/root/reference/proj/include/femlite/): assemble_blockwise / assemble
-(assembly.hpp:461,502), assemble_load (system.hpp:71), partition_boundary
+(assembly.hpp:261,302), assemble_load (system.hpp:71), partition_boundary
 (system.hpp:50), apply_neumann (system.hpp:123), apply_dirichlet
 (system.hpp:182), submatrix (sparse.hpp:159), plus ``assemble_system`` -- the
 fused pre-solve sequence of solve_poisson (solver.hpp:226-242) in one pass.
@@ -28,7 +28,7 @@ TET4_A = 0.58541019662496845
 TET4_B = 0.13819660112501051
 
 
-class AssemblyStrategy(enum.IntEnum):  # assembly.hpp:241 + the GPU tag
+class AssemblyStrategy(enum.IntEnum):  # assembly.hpp:41 + the GPU tag
     dense_oracle = 0
     triplet_loop = 1
     blockwise = 2
@@ -241,7 +241,7 @@ def run(mesh: Mesh, what: int, f=None, coef=None, g_dirichlet=None, g_neumann=No
 # ---------------------------------------------------------------------------
 def assemble_blockwise(mesh: Mesh, symmetric_fill: bool = False, coef=None,
                        ctx: Optional[Context] = None) -> CscMatrix:
-    """assembly.hpp:461.  ``symmetric_fill`` only changes the reference's triplet
+    """assembly.hpp:261.  ``symmetric_fill`` only changes the reference's triplet
     multiset; the GPU path always produces the default result."""
     if symmetric_fill:
         raise Error(ErrorCode.invalid_parameter,
@@ -250,7 +250,7 @@ def assemble_blockwise(mesh: Mesh, symmetric_fill: bool = False, coef=None,
 
 
 def assemble(mesh: Mesh, strategy=AssemblyStrategy.b200, ctx: Optional[Context] = None) -> CscMatrix:
-    """assembly.hpp:502: the blockwise strategy (and the b200 tag) run on the GPU;
+    """assembly.hpp:302: the blockwise strategy (and the b200 tag) run on the GPU;
     the dense/triplet cross-check oracles stay in the reference."""
     strategy = AssemblyStrategy(strategy)
     if strategy in (AssemblyStrategy.blockwise, AssemblyStrategy.b200):

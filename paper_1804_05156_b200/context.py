@@ -41,6 +41,12 @@ class Context:
         _lib.check(_lib.lib().fl_last_timings(self._h, buf), "fl_last_timings")
         return list(buf)
 
+    def last_kernel_timings(self):
+        """[element records, column kernel, placement] ms of the last assembly (FL_PROFILE=1)."""
+        buf = (C.c_double * 3)()
+        _lib.check(_lib.lib().fl_last_kernel_timings(self._h, buf), "fl_last_kernel_timings")
+        return list(buf)
+
     def close(self):
         if self._h:
             _lib.lib().fl_destroy(self._h)

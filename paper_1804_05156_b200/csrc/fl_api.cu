@@ -208,6 +208,12 @@ FL_API int fl_last_timings(const fl_ctx* ctx, double* ms4) {
     return FL_OK;
 }
 
+FL_API int fl_last_kernel_timings(const fl_ctx* ctx, double* ms3) {
+    if (!ctx || !ms3) return set_error(FL_ERR_ARGUMENT, "null argument");
+    for (int i = 0; i < 3; ++i) ms3[i] = ctx->ktimings[i];
+    return FL_OK;
+}
+
 // ---- mesh -----------------------------------------------------------------------
 FL_API int fl_mesh_create(fl_ctx* ctx, int dim, int32_t n_nodes, int32_t n_elems,
                           const double* nodes, const int32_t* elems, const int8_t* bd_flags,
@@ -285,6 +291,7 @@ FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     mesh->inc_ptr.release();
     mesh->inc.release();
     mesh->cursor.release();
+    mesh->emark.release();
     mesh->stats.release();
     delete mesh;
     return FL_OK;
@@ -387,6 +394,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     const cudaStream_t s = ctx->stream;
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[0], s));
     ctx->plan_timed = false;
+    ctx->kernel_timed = false;
     if (!mesh->planned && (what & (FL_OUT_STIFFNESS | FL_OUT_LOAD))) {
         FL_TRY(fl_mesh_plan(ctx, mesh));
         ctx->plan_timed = true;
@@ -482,6 +490,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         p.is_dir = res->is_dir.as<int8_t>();
         p.is_neu = res->is_neu.as<int8_t>();
         p.fidx = res->fidx.as<int32_t>();
+        p.emark = NC < N ? mesh->emark.as<uint8_t>() : nullptr;
         // free nodes below the range = free_rank[C0] (k_partition's exclusive scan)
         p.f_begin = (C0 > 0 && want_sys) ? res->fidx.as<int32_t>() + n1 + C0 : nullptr;
         p.col_ptr = res->arr[FL_A_COL_PTR].as<int32_t>();
@@ -582,6 +591,16 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
             ctx->timings[1] = b;
             ctx->timings[2] = c;
             ctx->timings[3] = a + b + c;
+            ctx->ktimings[0] = ctx->ktimings[1] = ctx->ktimings[2] = 0.0;
+            if (ctx->kernel_timed) {
+                float e = 0, f = 0, g = 0;
+                cudaEventElapsedTime(&e, ctx->ev[5], ctx->ev[6]);
+                cudaEventElapsedTime(&f, ctx->ev[6], ctx->ev[7]);
+                cudaEventElapsedTime(&g, ctx->ev[7], ctx->ev[3]);
+                ctx->ktimings[0] = e;
+                ctx->ktimings[1] = f;
+                ctx->ktimings[2] = g;
+            }
             ctx->timing_pending = false;
         }
         if (e & DERR_INDEX) return set_error(FL_E_INDEX_OUT_OF_RANGE, "element vertex index out of range");
@@ -630,6 +649,14 @@ static int64_t array_bytes(const fl_result* r, int which) {
     case FL_B_F: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n_free_cols : 0;
     }
     return -1;
+}
+
+FL_API int fl_result_counts_async(fl_result* res, int64_t* dev_out) {
+    if (!res || !dev_out || !res->ctx) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (!(res->what & (FL_OUT_STIFFNESS | FL_OUT_LOAD)))
+        return set_error(FL_ERR_ARGUMENT, "result holds no assembly");
+    FL_CUDA(cudaSetDevice(res->ctx->device));
+    return launch_result_counts(res->ctx, res, dev_out);
 }
 
 FL_API int fl_result_device_ptr(fl_result* res, int which, const void** ptr, int64_t* bytes) {
@@ -756,13 +783,33 @@ static double host_field(int kind, double value, double x, double y, double z) {
     return 0.0;
 }
 
-FL_API int fl_host_sample(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
-                          const int32_t* elems, int rule, int kind, double value, double* out) {
-    if ((dim != 2 && dim != 3) || !out || (n_nodes > 0 && !nodes) || (n_elems > 0 && !elems))
-        return set_error(FL_ERR_ARGUMENT, "bad argument");
-    const int nv = dim + 1;
+// Cartesian point q of element t under `rule` (the reference's formulas)
+static void host_point(int rule, int dim, const double* nodes, const int32_t* v, int q, double x[3]) {
     static const int tri[3][2] = {{1, 2}, {2, 0}, {0, 1}};
     static const int tet[4][3] = {{1, 3, 2}, {0, 2, 3}, {0, 3, 1}, {0, 1, 2}};
+    auto P = [&](int32_t k, int c) { return c < dim ? nodes[(size_t)k * dim + c] : 0.0; };
+    x[0] = x[1] = x[2] = 0.0;
+    if (rule == 0 && dim == 2) {  // system.hpp:86-90
+        for (int c = 0; c < 2; ++c) x[c] = (P(v[tri[q][0]], c) + P(v[tri[q][1]], c)) / 2.0;
+    } else if (rule == 0) {  // system.hpp:103-107
+        for (int k = 0; k < 4; ++k) {
+            const double lam = (k == q) ? 0.58541019662496845 : 0.13819660112501051;
+            for (int c = 0; c < 3; ++c) x[c] += lam * P(v[k], c);
+        }
+    } else if (dim == 2) {  // system.hpp:143
+        for (int c = 0; c < 2; ++c) x[c] = (P(v[tri[q][0]], c) + P(v[tri[q][1]], c)) / 2.0;
+    } else {  // system.hpp:160-161
+        for (int c = 0; c < 3; ++c)
+            x[c] = (P(v[tet[q][0]], c) + P(v[tet[q][1]], c) + P(v[tet[q][2]], c)) / 3.0;
+    }
+}
+
+FL_API int fl_host_sample(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                          const int32_t* elems, int rule, int kind, double value, double* out) {
+    if ((dim != 2 && dim != 3) || !out || (n_nodes > 0 && !nodes) || (n_elems > 0 && !elems) ||
+        rule < 0 || rule > 3)
+        return set_error(FL_ERR_ARGUMENT, "bad argument");
+    const int nv = dim + 1;
     auto P = [&](int32_t k, int c) { return c < dim ? nodes[(size_t)k * dim + c] : 0.0; };
     if (rule == 2) {
         for (int32_t k = 0; k < n_nodes; ++k) out[k] = host_field(kind, value, P(k, 0), P(k, 1), P(k, 2));
@@ -779,23 +826,22 @@ FL_API int fl_host_sample(int dim, int32_t n_nodes, int32_t n_elems, const doubl
             continue;
         }
         for (int q = 0; q < nv; ++q) {
-            double x[3] = {0.0, 0.0, 0.0};
-            if (rule == 0 && dim == 2) {  // system.hpp:86-90
-                for (int c = 0; c < 2; ++c) x[c] = (P(v[tri[q][0]], c) + P(v[tri[q][1]], c)) / 2.0;
-            } else if (rule == 0) {  // system.hpp:103-107
-                for (int k = 0; k < 4; ++k) {
-                    const double lam = (k == q) ? 0.58541019662496845 : 0.13819660112501051;
-                    for (int c = 0; c < 3; ++c) x[c] += lam * P(v[k], c);
-                }
-            } else if (dim == 2) {  // system.hpp:143
-                for (int c = 0; c < 2; ++c) x[c] = (P(v[tri[q][0]], c) + P(v[tri[q][1]], c)) / 2.0;
-            } else {  // system.hpp:160-161
-                for (int c = 0; c < 3; ++c)
-                    x[c] = (P(v[tet[q][0]], c) + P(v[tet[q][1]], c) + P(v[tet[q][2]], c)) / 3.0;
-            }
+            double x[3];
+            host_point(rule, dim, nodes, v, q, x);
             out[(size_t)t * nv + q] = host_field(kind, value, x[0], x[1], x[2]);
         }
     }
+    return FL_OK;
+}
+
+FL_API int fl_host_points(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                          const int32_t* elems, int rule, double* xyz) {
+    if ((dim != 2 && dim != 3) || !xyz || (n_nodes > 0 && !nodes) || (n_elems > 0 && !elems) ||
+        (rule != 0 && rule != 3))
+        return set_error(FL_ERR_ARGUMENT, "bad argument");
+    const int nv = dim + 1;
+    for (int32_t t = 0; t < n_elems; ++t)
+        for (int q = 0; q < nv; ++q) host_point(rule, dim, nodes, elems + (size_t)t * nv, q, xyz + ((size_t)t * nv + q) * 3);
     return FL_OK;
 }
 

@@ -5,7 +5,7 @@
 //   1. the tile's incidence keys (j << 30 | t) -> smem, unsorted from the plan;
 //   2. lane per incidence: rank of the key inside its column = the (j, t) order in
 //      which the reference's blockwise triplets reach that column
-//      (assembly.hpp:486-498 + the stable passes sparse.hpp:79-89); element
+//      (assembly.hpp:286-298 + the stable passes sparse.hpp:79-89); element
 //      geometry for column j (fl_geometry.cuh) -> s_ij (i = 0..d) and the load
 //      share, stored at [rank][i][column] (column-interleaved: conflict-free);
 //   3. P threads per column; thread u owns the distinct rows whose hash selects u

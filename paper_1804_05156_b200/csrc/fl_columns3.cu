@@ -6,7 +6,7 @@
 //   1. lane g < m loads incidence key g of c (j << 30 | t, unsorted from the
 //      plan) and the group bitonic-sorts the keys: lane g then holds the g-th
 //      incidence in (j, t) order -- the order in which the reference's
-//      blockwise triplets reach column c (assembly.hpp:486-498 after the stable
+//      blockwise triplets reach column c (assembly.hpp:286-298 after the stable
 //      passes sparse.hpp:79-89);
 //   2. each lane reads its incidence's 64-byte element record (k_elem_records:
 //      s_ij for i = 0..d, the load share, the vertices; FMA-free, exact
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
     for (int64_t t0 = (int64_t)blockIdx.x * kElemThreads; t0 < p.n_elems;
          t0 += (int64_t)gridDim.x * kElemThreads) {
         const int64_t t = t0 + threadIdx.x;
-        if (t < p.n_elems) {
+        if (t < p.n_elems && (!p.emark || p.emark[t])) {
             int32_t V[NV];
             if constexpr (D == 3) {
                 const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
@@ -468,6 +468,10 @@ template <int D, int L, bool PRE>
 static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     using C = V3<D, L>;
     FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
+    if (ctx->profile) {
+        FL_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+        ctx->kernel_timed = true;
+    }
     if constexpr (PRE) {
         const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
         FL_TRY(res->erec[0].ensure((size_t)64 * ne * (D + 1)));
@@ -485,9 +489,11 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS,
                              (int64_t)ctx->sm_count * std::max(per_sm, 1)));
+    if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
     k_columns3<D, L, PRE><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
+    if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
     return finish_staging(ctx, p, C::WTC);
 }
 

@@ -21,7 +21,7 @@ struct FieldDesc {
     const double* samples;
 };
 
-// built-in fields at a point (z = 0 in 2-D, mesh.hpp:111-116)
+// built-in fields at a point (z = 0 in 2-D, mesh.hpp:72-77)
 __device__ __forceinline__ double eval_point(const FieldDesc& f, double x, double y, double z) {
     switch (f.kind) {
     case FL_FIELD_CONST: return f.value;
@@ -38,8 +38,8 @@ template <int D>
 struct ElemCol;
 
 // ---------------------------------------------------------------------------
-// 2-D: assembly.hpp:333-351 (edge vectors, area, rotated normals),
-//      assembly.hpp:483-492 (s = n_i.n_j / (4 area)), system.hpp:80-96 (load)
+// 2-D: assembly.hpp:133-151 (edge vectors, area, rotated normals),
+//      assembly.hpp:283-292 (s = n_i.n_j / (4 area)), system.hpp:80-96 (load)
 // ---------------------------------------------------------------------------
 template <>
 struct ElemCol<2> {
@@ -96,7 +96,7 @@ struct ElemCol<2> {
         if (f.kind == FL_FIELD_NONE) return 0.0;
         const double ex1 = x[0] - x[2], ey1 = y[0] - y[2];
         const double ex2 = x[1] - x[0], ey2 = y[1] - y[0];
-        const double area = fabs(0.5 * (-ex2 * ey1 + ey2 * ex1));  // mesh.hpp:73-77
+        const double area = fabs(0.5 * (-ex2 * ey1 + ey2 * ex1));  // mesh.hpp:34-38
         const int i1 = (j + 1) % 3, i2 = (j + 2) % 3;
         double fa, fb;
         if (f.kind == FL_FIELD_SAMPLES) {
@@ -140,12 +140,12 @@ struct ElemCol<2> {
 };
 
 // ---------------------------------------------------------------------------
-// 3-D: assembly.hpp:352-369 (face normals by cross products, volume),
-//      assembly.hpp:483-492 (s = n_i.n_j / (36 vol)), system.hpp:97-111 (tet4 load)
+// 3-D: assembly.hpp:152-169 (face normals by cross products, volume),
+//      assembly.hpp:283-292 (s = n_i.n_j / (36 vol)), system.hpp:97-111 (tet4 load)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cross3(double ux, double uy, double uz, double vx, double vy,
                                        double vz, double& ox, double& oy, double& oz) {
-    // assembly.hpp:276-280
+    // assembly.hpp:76-80
     ox = uy * vz - uz * vy;
     oy = uz * vx - ux * vz;
     oz = ux * vy - uy * vx;
@@ -176,7 +176,7 @@ struct ElemCol<3> {
         }
     }
 
-    // |cr . v14| / 6 with cr = n_3 (same inputs as assembly.hpp:366), v14 = v3 - v0
+    // |cr . v14| / 6 with cr = n_3 (same inputs as assembly.hpp:166), v14 = v3 - v0
     __device__ __forceinline__ double volume(const double n3[3], const Recip& R6) const {
         const double d = n3[0] * (x[3] - x[0]) + n3[1] * (y[3] - y[0]) + n3[2] * (z[3] - z[0]);
         return div_by(fabs(d), R6);

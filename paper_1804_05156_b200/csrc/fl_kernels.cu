@@ -4,7 +4,7 @@
 //   plan    k_inc_count -> scan -> k_inc_fill -> k_inc_sort -> k_plan_stats
 //           node -> incidence lists sorted by (local index j, element t): the
 //           order in which the reference's blockwise triplets reach a column
-//           (assembly.hpp:486-498 + the stable counting sorts sparse.hpp:79-89).
+//           (assembly.hpp:286-298 + the stable counting sorts sparse.hpp:79-89).
 //   mark    k_mark_boundary -> scan -> k_partition (partition_boundary, system.hpp:50-67)
 //   column  k_columns<D>: one warp per output column c = one reference CSC column,
 //           exact per-entry summation order (i, j, t), zero drop, fused load
@@ -42,7 +42,8 @@ __global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin,
 
 __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
                            const int32_t* __restrict__ elems, const int32_t* __restrict__ inc_ptr,
-                           int32_t* __restrict__ cursor, uint32_t* __restrict__ inc) {
+                           int32_t* __restrict__ cursor, uint32_t* __restrict__ inc,
+                           uint8_t* __restrict__ emark) {
     const int64_t n_entries = (int64_t)n_elems * nv;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -54,6 +55,7 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_b
         const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
         const int32_t pos = __ldg(inc_ptr + lv) + atomicAdd(cursor + lv, 1);
         inc[pos] = (j << 30) | (uint32_t)t;
+        if (emark) emark[t] = 1;
     }
 }
 
@@ -101,7 +103,7 @@ __global__ void k_plan_stats(int32_t n_cols, int32_t n_nodes, int dim,
 }
 
 // ===========================================================================
-// validation (make_mesh, mesh.hpp:187-226)
+// validation (make_mesh, mesh.hpp:148-187)
 // ===========================================================================
 template <int D>
 __global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __restrict__ nodes,
@@ -130,7 +132,7 @@ __global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __res
             const double* a = nodes + 2 * (size_t)v[0];
             const double* b = nodes + 2 * (size_t)v[1];
             const double* c = nodes + 2 * (size_t)v[2];
-            // mesh.hpp:73-77
+            // mesh.hpp:34-38
             const double e2x = a[0] - c[0], e2y = a[1] - c[1];
             const double e3x = b[0] - a[0], e3y = b[1] - a[1];
             m = 0.5 * (-e3x * e2y + e3y * e2x);
@@ -139,7 +141,7 @@ __global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __res
             const double* p2 = nodes + 3 * (size_t)v[1];
             const double* p3 = nodes + 3 * (size_t)v[2];
             const double* p4 = nodes + 3 * (size_t)v[NV - 1];
-            // mesh.hpp:81-90 (division by 6 keeps the sign: test the numerator)
+            // mesh.hpp:42-51 (division by 6 keeps the sign: test the numerator)
             const double ax = p2[0] - p1[0], ay = p2[1] - p1[1], az = p2[2] - p1[2];
             const double bx = p3[0] - p1[0], by = p3[1] - p1[1], bz = p3[2] - p1[2];
             const double cx = p4[0] - p1[0], cy = p4[1] - p1[1], cz = p4[2] - p1[2];
@@ -154,7 +156,7 @@ __global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __res
 
 // ===========================================================================
 // boundary marking: partition_boundary (system.hpp:50-67) / boundary_faces
-// (mesh.hpp:261-285).  is_dir[v] = 1 for every vertex of a flag-1 face.
+// (mesh.hpp:222-246).  is_dir[v] = 1 for every vertex of a flag-1 face.
 // ===========================================================================
 template <int D>
 __global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ elems,
@@ -425,7 +427,7 @@ __device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lan
         }
         __syncwarp();
         if (lane == 0) {
-            // face-major order (lf, t) (mesh.hpp:268-283), accumulate from 0.0
+            // face-major order (lf, t) (mesh.hpp:229-244), accumulate from 0.0
             const int n = min(s_nneu[w], kMaxNeu);
             double add = 0.0;
             uint32_t last = 0;
@@ -764,9 +766,16 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         mesh->inc_ptr.as<int32_t>(), ctx->scan_ws.p, s));
     count_launch(ctx);
     FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)nc + 1), s));
+    uint8_t* emark = nullptr;
+    if (nc < N) {  // sharded: mark the elements the owned columns touch
+        FL_TRY(mesh->emark.ensure((size_t)std::max<int32_t>(mesh->n_elems, 1)));
+        emark = mesh->emark.as<uint8_t>();
+        FL_CUDA(cudaMemsetAsync(emark, 0, (size_t)mesh->n_elems, s));
+    }
     if (n_entries > 0) {
         k_inc_fill<<<grid, 256, 0, s>>>(mesh->n_elems, nv, N, c0, nc, mesh->elems.as<int32_t>(),
-                                        mesh->inc_ptr.as<int32_t>(), cnt, mesh->inc.as<uint32_t>());
+                                        mesh->inc_ptr.as<int32_t>(), cnt, mesh->inc.as<uint32_t>(),
+                                        emark);
         count_launch(ctx);
     }
     if (nc > 0) {
@@ -787,6 +796,30 @@ int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh) {
                                                             mesh->inc.as<uint32_t>());
         count_launch(ctx);
     }
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// {n_cols, n_free_cols, nnz, nnz_ff} of a result, on the device (no host sync)
+__global__ void k_result_counts(int32_t n_cols, int32_t col_begin, int32_t n_rows, int want_a,
+                                int want_sys, const int32_t* __restrict__ col_ptr,
+                                const int32_t* __restrict__ free_rank,
+                                const int32_t* __restrict__ ff_col_ptr, int64_t* __restrict__ out) {
+    const int32_t nf = want_sys ? free_rank[col_begin + n_cols] - free_rank[col_begin] : 0;
+    out[0] = n_cols;
+    out[1] = nf;
+    out[2] = want_a ? col_ptr[n_cols] : 0;
+    out[3] = want_sys ? ff_col_ptr[nf] : 0;
+    (void)n_rows;
+}
+
+int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out) {
+    const bool want_a = res->what & FL_OUT_STIFFNESS, want_sys = res->what & FL_OUT_SYSTEM;
+    k_result_counts<<<1, 1, 0, ctx->stream>>>(
+        res->n, res->col_begin, res->m, want_a, want_sys, res->arr[FL_A_COL_PTR].as<int32_t>(),
+        want_sys ? res->fidx.as<int32_t>() + (size_t)res->m + 1 : nullptr,
+        res->arr[FL_AFF_COL_PTR].as<int32_t>(), dev_out);
+    count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;
 }

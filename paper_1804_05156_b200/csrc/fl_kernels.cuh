@@ -57,6 +57,7 @@ struct ColParams {
     // (t, j) at srec + (t*(d+1) + j)*8: s_0j..s_dj, load share, the d+1 vertices
     double* srec;
     double* lrec;  // unused
+    const uint8_t* emark;  // sharded: records only for elements touching owned columns
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
@@ -78,6 +79,7 @@ int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
 int finish_staging(fl_ctx* ctx, ColParams& p, int tc);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
+int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out);
 size_t column_smem_bytes();
 int column_tile_width();
 

@@ -1,15 +1,15 @@
 """Mesh data model and canonical meshes (mesh.hpp).
 
-``Mesh`` mirrors ``femlite::Mesh`` (mesh.hpp:99-135): the immutable triple
+``Mesh`` mirrors ``femlite::Mesh`` (mesh.hpp:60-96): the immutable triple
 (nodes, elems, bd_flags) with zero-based int32 connectivity and one int8 flag
 per element face (face f opposite local vertex f).  The arrays live on the
 host; ``Mesh.device(ctx)`` uploads them once to an ``fl_mesh`` (device
 buffers + the cached topology plan) that every assembly call reuses.
 
 ``make_mesh`` validates on the GPU (fl_mesh_validate: index range, flag values,
-positive signed measure -- mesh.hpp:187-226).  The generators and boundary
+positive signed measure -- mesh.hpp:148-187).  The generators and boundary
 flagging are input preparation, vectorised numpy restatements
-of mesh.hpp:290-444 that are checked against the reference in tests.
+of mesh.hpp:251-405 that are checked against the reference in tests.
 """
 from __future__ import annotations
 
@@ -22,12 +22,12 @@ from . import _lib
 from .context import Context
 from .errors import Error, ErrorCode
 
-# mesh.hpp:68-69
+# mesh.hpp:29-30
 TRI_FACES = np.array([[1, 2], [2, 0], [0, 1]], dtype=np.int64)
 TET_FACES = np.array([[1, 3, 2], [0, 2, 3], [0, 3, 1], [0, 1, 2]], dtype=np.int64)
 
 
-class MeshShape(enum.IntEnum):  # mesh.hpp:345
+class MeshShape(enum.IntEnum):  # mesh.hpp:306
     unit_square = 0
     unit_cube = 1
     lshape = 2
@@ -43,7 +43,7 @@ class Mesh:
         self.bd_flags = np.ascontiguousarray(np.asarray(bd_flags, dtype=np.int8).reshape(self.elems.shape))
         self._dev = {}
 
-    # mesh.hpp:101-103
+    # mesh.hpp:62-64
     def num_nodes(self) -> int:
         return int(self.nodes.shape[0])
 
@@ -111,7 +111,7 @@ class DeviceMesh:
 
 
 def make_mesh(dim: int, nodes, elems, bd_flags=None, ctx: Context | None = None) -> Mesh:
-    """mesh.hpp:213-226: validate the raw arrays (on the GPU) and build a Mesh."""
+    """mesh.hpp:174-187: validate the raw arrays (on the GPU) and build a Mesh."""
     if dim not in (2, 3):
         raise Error(ErrorCode.invalid_parameter, "mesh dimension must be 2 or 3")
     nodes = np.asarray(nodes, dtype=np.float64).ravel()
@@ -128,7 +128,7 @@ def make_mesh(dim: int, nodes, elems, bd_flags=None, ctx: Context | None = None)
 
 
 # ---------------------------------------------------------------------------
-# generators (mesh.hpp:349-444), vectorised
+# generators (mesh.hpp:310-405), vectorised
 # ---------------------------------------------------------------------------
 def _unit_square(n: int):
     h = 1.0 / n
@@ -183,7 +183,7 @@ def _lshape(n: int):
     used[1:, 1:] |= kept
     remap = -np.ones((m + 1, m + 1), dtype=np.int64)
     remap[used] = np.arange(int(used.sum()))
-    gj, gi = np.nonzero(used)  # row-major: j outer, i inner -- mesh.hpp:422-432 order
+    gj, gi = np.nonzero(used)  # row-major: j outer, i inner -- mesh.hpp:383-393 order
     nodes = np.stack([-1.0 + gi * h, -1.0 + gj * h], axis=1)
     kj, ki = np.nonzero(kept)
     v00, v10 = remap[kj, ki], remap[kj, ki + 1]
@@ -195,7 +195,7 @@ def _lshape(n: int):
 
 
 def generate_mesh(shape, n: int) -> Mesh:
-    """mesh.hpp:449-458: canonical meshes, all flags zero."""
+    """mesh.hpp:410-419: canonical meshes, all flags zero."""
     if n < 1:
         raise Error(ErrorCode.invalid_parameter, "subdivision count must be >= 1")
     shape = MeshShape(shape)
@@ -210,7 +210,7 @@ def generate_mesh(shape, n: int) -> Mesh:
 
 
 # ---------------------------------------------------------------------------
-# boundary flagging (mesh.hpp:290-343)
+# boundary flagging (mesh.hpp:251-304)
 # ---------------------------------------------------------------------------
 def face_vertices(mesh: Mesh) -> np.ndarray:
     """[NT, d+1, d]: vertices of face f of every element (kTriFaces/kTetFaces order)."""
@@ -249,7 +249,7 @@ def _classify(mesh: Mesh, mask: np.ndarray, classifier) -> np.ndarray:
     table = TRI_FACES if d == 2 else TET_FACES
     verts = mesh.elems[t[:, None], table[lf]]  # [M, d]
     cen = []
-    for c in range(d):  # mesh.hpp:327-333: sum over face vertices from 0.0, then / d
+    for c in range(d):  # mesh.hpp:288-294: sum over face vertices from 0.0, then / d
         acc = np.zeros(t.size)
         for k in range(d):
             acc = acc + mesh.nodes[verts[:, k], c]

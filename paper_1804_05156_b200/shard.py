@@ -8,7 +8,7 @@ plan and the column kernel to the range).  The only exchange is one
 all_gather of the per-shard counts (n_cols, n_free_cols, nnz, nnz_ff), from
 which each rank learns its global offsets: concatenating the shards in rank
 order, with col_ptr shifted by the nnz of the ranks before, is bit-for-bit the
-reference's single CSC (assembly.hpp:461-500, sparse.hpp:72-110), because every
+reference's single CSC (assembly.hpp:261-300, sparse.hpp:72-110), because every
 column is computed from the same items in the same order whichever rank owns
 it.  A(free, free) and b_f shard the same way over the free columns.
 

@@ -22,7 +22,7 @@ def _signed(dim, nodes, elems):
 
 
 def fix_orientation(dim, nodes, elems):
-    """mesh.hpp:238-257: swap the last two vertices of negatively oriented elements."""
+    """mesh.hpp:199-218: swap the last two vertices of negatively oriented elements."""
     elems = elems.copy()
     neg = _signed(dim, nodes, elems) < 0
     elems[neg, dim - 1], elems[neg, dim] = elems[neg, dim].copy(), elems[neg, dim - 1].copy()

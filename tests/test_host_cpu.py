@@ -141,3 +141,14 @@ def test_stitch_rejects_unshifted_shard():
     from paper_1804_05156_b200.shard import stitch_csc
     with pytest.raises(ValueError):
         stitch_csc(3, [(np.array([1, 2]), np.array([0]), np.array([1.0]))])
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include/femlite"),
+                    reason="reference headers absent")
+def test_adapter_header_compiles_against_reference():
+    import subprocess
+    r = subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
+                        "-I/root/reference/proj/include", f"-I{ROOT}/include",
+                        os.path.join(ROOT, "oracle", "adapter_check.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

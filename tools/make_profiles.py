@@ -1,0 +1,43 @@
+"""Write profiles/ summaries from gpurun_out/ ncu exports.
+
+  python tools/make_profiles.py <round-tag> CONFIG...
+reads gpurun_out/ll_<cfg>.csv (launch lists: gpu__time_duration.sum +
+dram bytes per kernel, one assemble_system step, ncu --clock-control none)
+and writes profiles/<tag>_launches_<cfg>.txt plus profiles/traffic.json
+(numeric-phase dram bytes per step, read by bench.py as roofline.traffic).
+"""
+import collections
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NUMERIC = ("k_elem_records", "k_columns", "k_stage_copy", "finish_staging")
+tag = sys.argv[1]
+traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+for c in sys.argv[2:]:
+    rows = [r for r in csv.reader(open(os.path.join(ROOT, "gpurun_out", f"ll_{c}.csv"))) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    d = collections.defaultdict(dict)
+    for r in rows[1:]:
+        d[(int(r[ii]), r[ki])][r[mi]] = float(r[vi].replace(",", ""))
+    tot = sum(m.get("gpu__time_duration.sum", 0) for m in d.values())
+    lines = [f"# {c}: one assemble_system step (FL_OUT_SYSTEM|plan), ncu --clock-control none,",
+             "# serialized cold-cache launches; time share is what matters, not the absolute",
+             f"{'id':>3} {'kernel':60s} {'time_us':>10} {'share':>6} {'dram_rd_MB':>11} {'dram_wr_MB':>11}"]
+    num_bytes, num_t = 0.0, 0.0
+    for (i, k), m in sorted(d.items()):
+        t = m.get("gpu__time_duration.sum", 0)
+        rd, wr = m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
+        lines.append(f"{i:3d} {k[:60]:60s} {t/1e3:10.1f} {100*t/tot:5.1f}% {rd/1e6:11.1f} {wr/1e6:11.1f}")
+        if any(s in k for s in NUMERIC):
+            num_bytes += rd + wr
+            num_t += t
+    lines.append(f"# total {tot/1e6:.3f} ms; numeric phase {num_t/1e6:.3f} ms, dram {num_bytes/1e9:.3f} GB")
+    open(os.path.join(ROOT, "profiles", f"{tag}_launches_{c}.txt"), "w").write("\n".join(lines) + "\n")
+    traffic[c] = {"dram_bytes": num_bytes, "source": f"profiles/{tag}_launches_{c}.txt (ncu dram__bytes_read.sum+write.sum, numeric-phase kernels)"}
+    print("\n".join(lines[-3:]))
+json.dump(traffic, open(traffic_path, "w"), indent=1)
