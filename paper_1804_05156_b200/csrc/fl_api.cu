@@ -292,6 +292,8 @@ FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     mesh->inc.release();
     mesh->cursor.release();
     mesh->emark.release();
+    mesh->bstage.release();
+    mesh->bcnt.release();
     mesh->stats.release();
     delete mesh;
     return FL_OK;

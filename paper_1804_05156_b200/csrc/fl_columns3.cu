@@ -14,11 +14,11 @@
 //   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
 //      A(c,c) = fold of s_jj in lane order (its items are exactly those): the
 //      shares are staged in smem and group lanes 0 / 1 run the two folds;
-//   4. off-diagonal items (i != j) are staged at itm[i][lane]; per pass i, lanes
-//      with the same row are found with match_any, the group leader inserts the
-//      row in the group's small smem hash (CAS) and stores the pass's lane mask
-//      for that slot; the slot's lane then folds its items pass by pass, lanes
-//      ascending = the reference's (i*(d+1)+j, t) order;
+//   4. off-diagonal items (i != j) are staged at itm[i][lane]; every lane inserts
+//      its rows into the group's small smem hash (CAS: equal rows meet on one
+//      slot) and sets its lane bit in the slot's pass-i mask (atomicOr); the
+//      slot's lane then folds its items pass by pass, lanes ascending = the
+//      reference's (i*(d+1)+j, t) order;
 //   5. slots ranked by row, exact zeros dropped (sparse.hpp:105), A(free,free)
 //      rows kept, all written to the tile staging (k_stage_copy places them).
 // Limits (fallback to the general kernel through DERR_V2_OVERFLOW): m > L, or
@@ -173,21 +173,38 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
         const int64_t sbase = tile * p.tile_cap;
         int run_a = 0, run_f = 0;  // warp-uniform: entries staged so far in this tile
         bool bad = false;
+        // the tile's column bounds: one inc_ptr load per lane (WTC <= 32), then
+        // shuffles; the next column's keys are prefetched one iteration ahead
+        const int32_t lc0 = (int32_t)(tile * C::WTC);
+        const int ncol_t = (int)min((int64_t)C::WTC, (int64_t)p.n_cols - lc0);
+        const int32_t ipl = lane <= ncol_t ? __ldg(p.inc_ptr + lc0 + lane) : 0;
+        const int32_t ipe = __ldg(p.inc_ptr + lc0 + ncol_t);
+        auto col_range = [&](int q, int32_t& p0, int32_t& m) {
+            const int32_t a = __shfl_sync(FULL, ipl, q & 31);
+            const int32_t b = __shfl_sync(FULL, ipl, (q + 1) & 31);
+            p0 = a;
+            m = q < ncol_t ? ((q + 1 >= ncol_t) ? ipe : b) - a : 0;
+        };
+        int32_t p0n, mn;
+        col_range(gi, p0n, mn);
+        uint32_t key_next = (g < mn && mn <= L) ? __ldg(p.inc + p0n + g) : 0xFFFFFFFFu;
         for (int it = 0; it < C::ITERS; ++it) {
-            const int32_t lc = (int32_t)(tile * C::WTC) + it * C::GPW + gi;  // owned column
-            const bool act = lc < p.n_cols;
+            const int q = it * C::GPW + gi;
+            const int32_t lc = lc0 + q;  // owned column
+            const bool act = q < ncol_t;
             const int32_t c = p.c_begin + lc;  // global node
-            int32_t p0 = 0, m = 0;
-            if (act) {
-                p0 = __ldg(p.inc_ptr + lc);
-                m = __ldg(p.inc_ptr + lc + 1) - p0;
+            int32_t m = mn;
+            uint32_t key = key_next;
+            if (it + 1 < C::ITERS) {
+                col_range(q + C::GPW, p0n, mn);
+                key_next = (g < mn && mn <= L) ? __ldg(p.inc + p0n + g) : 0xFFFFFFFFu;
             }
             if (m > L) {
                 bad = true;
                 m = 0;
+                key = 0xFFFFFFFFu;
             }
             // ---- 1. keys, sorted ascending inside the group
-            uint32_t key = (g < m) ? __ldg(p.inc + p0 + g) : 0xFFFFFFFFu;
 #pragma unroll
             for (int k = 2; k <= L; k <<= 1) {
 #pragma unroll
@@ -277,20 +294,20 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
             if (g < 2) {
                 const double* src = g == 0 ? sm.lb : sm.ld;
                 const double2* src2 = reinterpret_cast<const double2*>(src);
-                int q = 0;
-                for (; q + 1 < m; q += 2) {
-                    const double2 v = src2[q >> 1];
+                const int np = m >> 1;
+#pragma unroll 2
+                for (int q = 0; q < np; ++q) {
+                    const double2 v = src2[q];
                     fold = fold + v.x;
                     fold = fold + v.y;
                 }
-                if (q < m) fold = fold + src[q];
+                if (m & 1) fold = fold + src[m - 1];
             }
             const double b = __shfl_sync(FULL, fold, 0, L);
             const double dg = __shfl_sync(FULL, fold, 1, L);
-            // ---- 4. off-diagonal items.  Item (i, lane) sits at itm[i][lane]; per
-            //      pass i the group leader of each row finds the row's slot (CAS
-            //      insert) and records the pass's lane mask msk[slot][i].  Slot h
-            //      then folds its items pass by pass, lanes ascending: the
+            // ---- 4. off-diagonal items.  Item (i, lane) sits at itm[i][lane]; its
+            //      row's slot (CAS insert) gets the lane's bit in msk[slot][i].
+            //      Slot h then folds its items pass by pass, lanes ascending: the
             //      reference's (i*(d+1)+j, t) order.
             if (p.want_a) {
                 for (int h = g; h < C::HS; h += L) {
@@ -303,31 +320,25 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < NV; ++i) {
-                    const bool has = valid && i != j;
-                    unsigned gm;
-                    if constexpr (L == 32) {  // one group per warp: rows need no group tag
-                        gm = __match_any_sync(FULL, has ? (uint32_t)R[i] : (0x80000000u | lane));
-                    } else {
-                        gm = __match_any_sync(FULL, has ? (((uint64_t)gi << 32) | (uint32_t)R[i])
-                                                        : ((1ull << 63) | (uint64_t)lane));
-                    }
-                    if (has && (gm & lower) == 0) {  // leader of this row in pass i
-                        const int32_t r = R[i];
-                        uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
-                        int slot = -1;
-                        for (int probe = 0; probe < C::HS; ++probe) {
-                            const int32_t old = atomicCAS(&sm.row[h], -1, r);
-                            if (old == -1 || old == r) {
-                                slot = (int)h;
-                                break;
-                            }
-                            h = (h + 1) & (C::HS - 1);
+                    if (!valid || i == j) continue;
+                    // every lane inserts its own row (equal rows meet on one slot: the
+                    // CAS returns the row) and sets its bit in the slot's pass-i mask;
+                    // the bit position is the lane, so atomic order does not matter
+                    const int32_t r = R[i];
+                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                    int slot = -1;
+                    for (int probe = 0; probe < C::HS; ++probe) {
+                        const int32_t old = atomicCAS(&sm.row[h], -1, r);
+                        if (old == -1 || old == r) {
+                            slot = (int)h;
+                            break;
                         }
-                        if (slot >= 0) reinterpret_cast<unsigned*>(&sm.msk[slot])[i] = gm >> (gi * L);
-                        else bad = true;
+                        h = (h + 1) & (C::HS - 1);
                     }
-                    __syncwarp();
+                    if (slot >= 0) atomicOr(reinterpret_cast<unsigned*>(&sm.msk[slot]) + i, 1u << g);
+                    else bad = true;
                 }
+                __syncwarp();
                 // ---- 5. the diagonal slot, the folds, rows ranked, zero drop
                 if (g == 0 && act && m > 0) {
                     uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
@@ -359,12 +370,20 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                         double acc = dg;
                         if (r != c) {
                             acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                            // bit b of the concatenated pass masks = item itm[b / L][b % L]:
+                            // ascending bits walk (i, lane) in the reference's order
                             const uint4 mk4 = sm.msk[h];
-                            const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
-#pragma unroll
-                            for (int i = 0; i < NV; ++i)
-                                for (unsigned mm = mk[i]; mm; mm &= mm - 1)
-                                    acc = acc + sm.itm[i][__ffs(mm) - 1];
+                            const double* flat = &sm.itm[0][0];
+                            uint64_t w0, w1 = 0;
+                            if constexpr (L == 32) {
+                                w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << 32);
+                                w1 = (uint64_t)mk4.z | ((uint64_t)mk4.w << 32);
+                            } else {
+                                w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) | ((uint64_t)mk4.z << (2 * L));
+                            }
+                            for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
+                            if constexpr (L == 32)
+                                for (uint64_t w = w1; w; w &= w - 1) acc = acc + flat[63 + __ffsll(w)];
                         }
                         int rk = 0;  // rows below r; unused entries (-1) compare as huge
                         const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
@@ -387,7 +406,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                 __syncwarp();
                 const bool col_free = act && p.want_sys && __ldg(p.fidx + c) >= 0;
                 int na = 0, nf = 0;
-                // compaction in chunks of L entries; pass 1: counts per group
+                // compaction in chunks of L entries; pass 1: counts per group (one
+                // group per warp: the column starts at the warp's running count)
+                if (L < 32)
                 for (int base = 0; base < C::MAXS; base += L) {
                     const int q = base + g;
                     const bool in = q < nslot;
@@ -409,9 +430,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                         pf += yf;
                     }
                 }
-                const int tot_a = __shfl_sync(FULL, pa, 31), tot_f = __shfl_sync(FULL, pf, 31);
+                int tot_a = __shfl_sync(FULL, pa, 31), tot_f = __shfl_sync(FULL, pf, 31);
                 int wa = run_a + pa - na, wf = run_f + pf - nf;  // this column's first slot
-                if (act && g == 0) {
+                if (L < 32 && act && g == 0) {
                     p.colcnt_a[lc] = wa + na;
                     if (p.want_sys) p.colcnt_f[lc] = wf + nf;
                 }
@@ -438,6 +459,14 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                     }
                     wa += __popc(ba);
                     wf += __popc(bf);
+                }
+                if (L == 32) {
+                    tot_a = wa - run_a;
+                    tot_f = wf - run_f;
+                    if (act && g == 0) {
+                        p.colcnt_a[lc] = wa;
+                        if (p.want_sys) p.colcnt_f[lc] = wf;
+                    }
                 }
                 run_a += tot_a;
                 run_f += tot_f;

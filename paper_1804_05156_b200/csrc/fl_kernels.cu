@@ -59,6 +59,101 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_b
     }
 }
 
+// ---- bucketed plan (large meshes).  Random node ids turn k_inc_fill's 4-byte
+// writes into sector-granular read-modify-writes over the whole incidence array.
+// Instead: (1) count per node AND per bucket of 2^shift consecutive nodes;
+// (2) partition the incidences by bucket into a staging array (block-local
+// smem ranks, one global atomic per bucket per block: coalesced runs);
+// (3) fill from the staging in bucket order, so the live destination range is
+// one bucket's slice of the incidence array, resident in L2.
+constexpr int kPlanBlock = 256, kPlanItems = 8, kMaxBuckets = 256;
+
+__global__ void __launch_bounds__(kPlanBlock)
+k_inc_count_b(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols, int shift,
+              const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
+              int32_t* __restrict__ bcnt, uint32_t* __restrict__ err) {
+    __shared__ int32_t hist[kMaxBuckets];
+    const int nb = ((n_cols - 1) >> shift) + 1;
+    for (int b = threadIdx.x; b < nb; b += kPlanBlock) hist[b] = 0;
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(elems + e);
+        if (v < 0 || v >= n_nodes) {
+            atomicOr(err, DERR_INDEX);
+            continue;
+        }
+        const uint32_t lv = (uint32_t)(v - c_begin);
+        if (lv < (uint32_t)n_cols) {
+            atomicAdd(cnt + lv, 1);
+            atomicAdd(&hist[lv >> shift], 1);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kPlanBlock)
+        if (hist[b]) atomicAdd(bcnt + b, hist[b]);
+}
+
+__global__ void __launch_bounds__(kPlanBlock)
+k_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
+                 int shift, const int32_t* __restrict__ elems, const int32_t* __restrict__ boff,
+                 int32_t* __restrict__ bcur, int2* __restrict__ stage) {
+    __shared__ int32_t hist[kMaxBuckets];
+    __shared__ int32_t base[kMaxBuckets];
+    const int nb = ((n_cols - 1) >> shift) + 1;
+    constexpr int CH = kPlanBlock * kPlanItems;
+    for (int64_t e0 = (int64_t)blockIdx.x * CH; e0 < n_entries; e0 += (int64_t)gridDim.x * CH) {
+        for (int b = threadIdx.x; b < nb; b += kPlanBlock) hist[b] = 0;
+        __syncthreads();
+        int32_t lv[kPlanItems], rk[kPlanItems];
+        uint32_t key[kPlanItems];
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k) {
+            const int64_t e = e0 + k * kPlanBlock + threadIdx.x;
+            lv[k] = -1;
+            if (e < n_entries) {
+                const int32_t v = __ldg(elems + e);
+                const uint32_t l = (uint32_t)(v - c_begin);
+                if (v >= 0 && v < n_nodes && l < (uint32_t)n_cols) {
+                    lv[k] = (int32_t)l;
+                    const int32_t t = (int32_t)(e / nv);
+                    key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
+                    rk[k] = atomicAdd(&hist[l >> shift], 1);
+                }
+            }
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += kPlanBlock)
+            if (hist[b]) base[b] = __ldg(boff + b) + atomicAdd(bcur + b, hist[b]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k)
+            if (lv[k] >= 0) stage[base[lv[k] >> shift] + rk[k]] = make_int2(lv[k], (int32_t)key[k]);
+        __syncthreads();
+    }
+}
+
+__global__ void k_bucket_offsets(int nb, int shift, int32_t n_cols, const int32_t* __restrict__ inc_ptr,
+                                 int32_t* __restrict__ boff) {
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        boff[b] = inc_ptr[min((int64_t)b << shift, (int64_t)n_cols)];
+}
+
+// total staged = inc_ptr[n_cols] (read on the device: no host sync in the plan)
+__global__ void __launch_bounds__(kPlanBlock)
+k_inc_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage,
+             const int32_t* __restrict__ inc_ptr, int32_t* __restrict__ cursor,
+             uint32_t* __restrict__ inc, uint8_t* __restrict__ emark) {
+    const int64_t n_staged = *total;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_staged;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int2 s = __ldg(stage + q);
+        const int32_t pos = __ldg(inc_ptr + s.x) + atomicAdd(cursor + s.x, 1);
+        inc[pos] = (uint32_t)s.y;
+        if (emark) emark[(uint32_t)s.y & 0x3FFFFFFFu] = 1;
+    }
+}
+
 // Sort each node's incidence keys ascending = (j, t) order.  Segments are
 // short (2-D ~6, 3-D Kuhn 24): insertion sort per thread.
 __global__ void k_inc_sort(int32_t n_nodes, const int32_t* __restrict__ inc_ptr,
@@ -756,7 +851,28 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
     FL_CUDA(cudaMemsetAsync(mesh->stats.p, 0, sizeof(unsigned long long) * 4, s));
     const int grid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256), 1),
                                             (int64_t)ctx->sm_count * 16);
-    if (n_entries > 0) {
+    uint8_t* emark = nullptr;
+    if (nc < N) {  // sharded: mark the elements the owned columns touch
+        FL_TRY(mesh->emark.ensure((size_t)std::max<int32_t>(mesh->n_elems, 1)));
+        emark = mesh->emark.as<uint8_t>();
+        FL_CUDA(cudaMemsetAsync(emark, 0, (size_t)mesh->n_elems, s));
+    }
+    // bucketed fill for large meshes (FL_PLAN=0|1 overrides)
+    const char* env = std::getenv("FL_PLAN");
+    const bool bucketed = nc > 0 && n_entries > 0 &&
+                          (env ? env[0] == '1' : n_entries >= ((int64_t)1 << 26));
+    int shift = 0;
+    while (((int64_t)(nc - 1) >> shift) + 1 > kMaxBuckets / 2) ++shift;
+    const int nb = nc > 0 ? ((nc - 1) >> shift) + 1 : 0;
+    int32_t* bcnt = nullptr;
+    if (bucketed) {
+        FL_TRY(mesh->bcnt.ensure(sizeof(int32_t) * 3 * (kMaxBuckets + 1)));
+        bcnt = mesh->bcnt.as<int32_t>();
+        FL_CUDA(cudaMemsetAsync(bcnt, 0, sizeof(int32_t) * 3 * (kMaxBuckets + 1), s));
+        k_inc_count_b<<<grid, kPlanBlock, 0, s>>>(n_entries, N, c0, nc, shift,
+                                                  mesh->elems.as<int32_t>(), cnt, bcnt, d_err);
+        count_launch(ctx);
+    } else if (n_entries > 0) {
         k_inc_count<<<grid, 256, 0, s>>>(n_entries, N, c0, nc, mesh->elems.as<int32_t>(), cnt, d_err);
         count_launch(ctx);
     }
@@ -766,13 +882,26 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         mesh->inc_ptr.as<int32_t>(), ctx->scan_ws.p, s));
     count_launch(ctx);
     FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)nc + 1), s));
-    uint8_t* emark = nullptr;
-    if (nc < N) {  // sharded: mark the elements the owned columns touch
-        FL_TRY(mesh->emark.ensure((size_t)std::max<int32_t>(mesh->n_elems, 1)));
-        emark = mesh->emark.as<uint8_t>();
-        FL_CUDA(cudaMemsetAsync(emark, 0, (size_t)mesh->n_elems, s));
-    }
-    if (n_entries > 0) {
+    if (bucketed) {
+        // bucket offsets = inc_ptr at the bucket boundaries
+        int32_t* boff = bcnt + (kMaxBuckets + 1);
+        int32_t* bcur = bcnt + 2 * (kMaxBuckets + 1);
+        const int32_t* ip = mesh->inc_ptr.as<int32_t>();
+        const int sh = shift;
+        const int32_t ncc = nc;
+        k_bucket_offsets<<<1, kMaxBuckets, 0, s>>>(nb, sh, ncc, ip, boff);
+        count_launch(ctx);
+        FL_TRY(mesh->bstage.ensure(sizeof(int2) * (size_t)n_entries));
+        int2* stage = mesh->bstage.as<int2>();
+        const int64_t chunks = (n_entries + kPlanBlock * kPlanItems - 1) / (kPlanBlock * kPlanItems);
+        const int g2 = (int)std::min<int64_t>(chunks, (int64_t)ctx->sm_count * 8);
+        k_bucket_scatter<<<g2, kPlanBlock, 0, s>>>(n_entries, nv, N, c0, nc, shift,
+                                                   mesh->elems.as<int32_t>(), boff, bcur, stage);
+        count_launch(ctx);
+        k_inc_fill_b<<<grid, kPlanBlock, 0, s>>>(ip + nc, stage, ip, cnt, mesh->inc.as<uint32_t>(),
+                                                 emark);
+        count_launch(ctx);
+    } else if (n_entries > 0) {
         k_inc_fill<<<grid, 256, 0, s>>>(mesh->n_elems, nv, N, c0, nc, mesh->elems.as<int32_t>(),
                                         mesh->inc_ptr.as<int32_t>(), cnt, mesh->inc.as<uint32_t>(),
                                         emark);

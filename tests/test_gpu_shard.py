@@ -118,3 +118,19 @@ def test_set_columns_rejects_bad_range(ctx):
         dm.set_columns(2, 1)
     with pytest.raises(fl.Error):
         dm.set_columns(0, g["nodes"].shape[0] + 1)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+@pytest.mark.parametrize("tag", ["square8_jit", "cube3_mixed_jit", "lshape4_jit"])
+def test_bucketed_plan_matches_golden(tag, world, ctx, monkeypatch):
+    """The bucketed plan (used for large meshes) forced on small ones."""
+    monkeypatch.setenv("FL_PLAN", "1")
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", tag + ".npz"))
+    m = _mesh(g)
+    parts = _shards(m, world, _lib.OUT_STIFFNESS | _lib.OUT_LOAD, ctx, f=1.0)
+    full = stitch_csc(m.num_nodes(), [(r.matrix().col_ptr, r.matrix().row_idx, r.matrix().values)
+                                      for _, r, _ in parts])
+    np.testing.assert_array_equal(full.col_ptr, g["a_col_ptr"])
+    np.testing.assert_array_equal(full.row_idx, g["a_row_idx"])
+    assert _bits(full.values) == _bits(g["a_values"])
+    assert _bits(np.concatenate([r.vector(_lib.B) for _, r, _ in parts])) == _bits(g["b_1"])
