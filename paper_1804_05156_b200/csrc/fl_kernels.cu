@@ -66,7 +66,7 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_b
 // smem ranks, one global atomic per bucket per block: coalesced runs);
 // (3) fill from the staging in bucket order, so the live destination range is
 // one bucket's slice of the incidence array, resident in L2.
-constexpr int kPlanBlock = 256, kPlanItems = 8, kMaxBuckets = 256;
+constexpr int kPlanBlock = 256, kPlanItems = 16, kMaxBuckets = 1024;
 
 __global__ void __launch_bounds__(kPlanBlock)
 k_inc_count_b(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols, int shift,
@@ -857,12 +857,17 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         emark = mesh->emark.as<uint8_t>();
         FL_CUDA(cudaMemsetAsync(emark, 0, (size_t)mesh->n_elems, s));
     }
-    // bucketed fill for large meshes (FL_PLAN=0|1 overrides)
+    // bucketed fill for large 2-D meshes (FL_PLAN=0|1 overrides).  Measured on
+    // B200 (profiles/r01_launches_C3/C5): C3 (100M incidences, 6 per node) plan
+    // 8.4 -> 4.9 ms; C5 (400M, 24 per node) 9.8 -> 11.9 ms, so 3-D keeps the
+    // direct fill, whose 96-byte per-node segments already batch the writes.
     const char* env = std::getenv("FL_PLAN");
     const bool bucketed = nc > 0 && n_entries > 0 &&
-                          (env ? env[0] == '1' : n_entries >= ((int64_t)1 << 26));
+                          (env ? env[0] == '1' : (mesh->dim == 2 && n_entries >= ((int64_t)1 << 26)));
+    // as many buckets of 2^shift nodes as the block histograms hold: a bucket's
+    // slice of the incidence array (~3 MB at C5) stays in L2 while it is filled
     int shift = 0;
-    while (((int64_t)(nc - 1) >> shift) + 1 > kMaxBuckets / 2) ++shift;
+    while (nc > 0 && ((int64_t)(nc - 1) >> shift) + 1 > kMaxBuckets) ++shift;
     const int nb = nc > 0 ? ((nc - 1) >> shift) + 1 : 0;
     int32_t* bcnt = nullptr;
     if (bucketed) {
