@@ -8,7 +8,7 @@
 //      incidence in (j, t) order -- the order in which the reference's
 //      blockwise triplets reach column c (assembly.hpp:286-298 after the stable
 //      passes sparse.hpp:79-89);
-//   2. each lane reads its incidence's 64-byte element record (k_elem_records:
+//   2. each lane reads its incidence from the 128-byte element record (k_elem_records:
 //      s_ij for i = 0..d, the load share, the vertices; FMA-free, exact
 //      division) -- or, with FL_KERNEL=3, computes them itself (fl_geometry.cuh);
 //   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
@@ -77,7 +77,7 @@ constexpr int kElemThreads = 128;
 template <int D>
 __global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
     constexpr int NV = D + 1;
-    constexpr int W = NV * 4 + 1;  // int4 words per element in smem (+1: no bank conflicts)
+    constexpr int W = 8 + 1;  // int4 words per element in smem (+1: no bank conflicts)
     __shared__ int4 stage[kElemThreads * W];
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
@@ -122,31 +122,30 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
                 if (p.want_b) ec.load_all((int32_t)t, meas, p.f, Lj);
                 else Lj[0] = Lj[1] = Lj[2] = Lj[3] = 0.0;
             }
-            // one 64-byte record per incidence (t, j): column j of the local matrix
-            // (= row j by symmetry), the load share, the vertices
+            // one 128-byte record per element: the upper triangle of the local
+            // matrix (s_ij == s_ji), the d+1 load shares, the vertex ids
+            double rec[16];
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < NV; ++a)
+#pragma unroll
+                for (int b = a; b < NV; ++b) rec[k++] = S[a][b];
+#pragma unroll
+            for (int a = 0; a < NV; ++a) rec[k++] = Lj[a];
+            for (; k < 14; ++k) rec[k] = 0.0;
             int4* st = stage + threadIdx.x * W;
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                double2 w0 = make_double2(S[j][0], S[j][1]);
-                double2 w1 = D == 3 ? make_double2(S[j][2], S[j][3]) : make_double2(S[j][2], Lj[j]);
-                double2 w2 = D == 3 ? make_double2(Lj[j], 0.0) : make_double2(0.0, 0.0);
-                st[4 * j] = *reinterpret_cast<int4*>(&w0);
-                st[4 * j + 1] = *reinterpret_cast<int4*>(&w1);
-                if constexpr (D == 3) {
-                    st[4 * j + 2] = *reinterpret_cast<int4*>(&w2);
-                    st[4 * j + 3] = make_int4(V[0], V[1], V[2], V[3]);
-                } else {
-                    st[4 * j + 2] = make_int4(V[0], V[1], V[2], 0);
-                    st[4 * j + 3] = make_int4(0, 0, 0, 0);
-                }
+            for (int q = 0; q < 7; ++q) {
+                double2 w = make_double2(rec[2 * q], rec[2 * q + 1]);
+                st[q] = *reinterpret_cast<int4*>(&w);
             }
+            st[7] = make_int4(V[0], V[1], V[2], D == 3 ? V[3] : 0);
         }
         __syncthreads();
         // coalesced write-out of the block's contiguous records
         const int64_t n = min((int64_t)kElemThreads, p.n_elems - t0);
-        int4* out = reinterpret_cast<int4*>(p.srec) + t0 * NV * 4;
-        for (int q = threadIdx.x; q < n * NV * 4; q += kElemThreads)
-            out[q] = stage[(q / (NV * 4)) * W + q % (NV * 4)];
+        int4* out = reinterpret_cast<int4*>(p.srec) + t0 * 8;
+        for (int q = threadIdx.x; q < n * 8; q += kElemThreads) out[q] = stage[(q >> 3) * W + (q & 7)];
         __syncthreads();
     }
 }
@@ -228,27 +227,19 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(
                 s[i] = 0.0;
             }
             if (valid && PRE) {
-                const double2* rec =
-                    reinterpret_cast<const double2*>(p.srec + ((size_t)t * NV + j) * 8);
-                const double2 a01 = __ldg(rec), a23 = __ldg(rec + 1);
-                s[0] = a01.x;
-                s[1] = a01.y;
-                s[2] = a23.x;
-                if constexpr (D == 3) {
-                    s[3] = a23.y;
-                    l = __ldg(rec + 2).x;
-                    const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 3);
-                    R[0] = e.x;
-                    R[1] = e.y;
-                    R[2] = e.z;
-                    R[3] = e.w;
-                } else {
-                    l = a23.y;
-                    const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 2);
-                    R[0] = e.x;
-                    R[1] = e.y;
-                    R[2] = e.z;
-                }
+                // the element's 128-byte record: s_ij at the upper-triangle slot of
+                // (min(i,j), max(i,j)), then the load shares, then the vertex ids
+                const double* rec = p.srec + (size_t)t * 16;
+                constexpr uint64_t TRI = D == 3 ? 0x9863875265413210ull   // slot of (i, j): 4 bits
+                                                : 0x0000054204310210ull;  // at 4 * (4j + i)
+#pragma unroll
+                for (int i = 0; i < NV; ++i) s[i] = __ldg(rec + ((TRI >> (4 * (4 * j + i))) & 15));
+                l = __ldg(rec + (D == 3 ? 10 : 6) + j);
+                const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 7);
+                R[0] = e.x;
+                R[1] = e.y;
+                R[2] = e.z;
+                if constexpr (D == 3) R[3] = e.w;
             } else if (valid) {
                 if constexpr (D == 3) {
                     const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
@@ -503,7 +494,7 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     }
     if constexpr (PRE) {
         const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
-        FL_TRY(res->erec[0].ensure((size_t)64 * ne * (D + 1)));
+        FL_TRY(res->erec[0].ensure((size_t)128 * ne));
         p.srec = res->erec[0].as<double>();
         p.lrec = nullptr;
         if (p.n_elems > 0) {

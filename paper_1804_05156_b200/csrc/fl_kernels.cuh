@@ -53,8 +53,8 @@ struct ColParams {
     int32_t* tile_off;   // [2][n_tiles + 1]: exclusive scans of tile_tot
     int32_t* colcnt_a;   // [N] in-tile inclusive count after column c
     int32_t* colcnt_f;   // [N] same for A(free, free) (indexed by column c)
-    // element-first records (k_elem_records): one 64-byte record per incidence
-    // (t, j) at srec + (t*(d+1) + j)*8: s_0j..s_dj, load share, the d+1 vertices
+    // element-first records (k_elem_records): one 128-byte record per element at
+    // srec + 16t: upper triangle of the local matrix, d+1 load shares, vertex ids
     double* srec;
     double* lrec;  // unused
     const uint8_t* emark;  // sharded: records only for elements touching owned columns
