@@ -25,18 +25,30 @@ namespace fl {
 // ===========================================================================
 // plan
 // ===========================================================================
+// Consecutive entries of element-ordered meshes repeat vertices (the tets of a
+// Kuhn cube share 8 vertices over 24 entries): lanes holding the same node are
+// grouped with match_any and the group leader issues one atomic for all of them.
 __global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
                             const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
                             uint32_t* __restrict__ err) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = __ldg(elems + e);
-        if (v < 0 || v >= n_nodes) {
-            atomicOr(err, DERR_INDEX);
-            continue;
+    const unsigned lower = (1u << (threadIdx.x & 31)) - 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // warp-uniform trip count: every lane reaches the match_any
+    const int64_t base = start - (threadIdx.x & 31);
+    for (int64_t e0 = base; e0 < n_entries; e0 += stride) {
+        const int64_t e = e0 + (threadIdx.x & 31);
+        int32_t key = -1;
+        if (e < n_entries) {
+            const int32_t v = __ldg(elems + e);
+            if (v < 0 || v >= n_nodes) {
+                atomicOr(err, DERR_INDEX);
+            } else if ((uint32_t)(v - c_begin) < (uint32_t)n_cols) {
+                key = v - c_begin;
+            }
         }
-        const uint32_t lv = (uint32_t)(v - c_begin);
-        if (lv < (uint32_t)n_cols) atomicAdd(cnt + lv, 1);
+        const unsigned g = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && (g & lower) == 0) atomicAdd(cnt + key, __popc(g));
     }
 }
 
@@ -44,18 +56,31 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_b
                            const int32_t* __restrict__ elems, const int32_t* __restrict__ inc_ptr,
                            int32_t* __restrict__ cursor, uint32_t* __restrict__ inc,
                            uint8_t* __restrict__ emark) {
+    (void)inc_ptr;
     const int64_t n_entries = (int64_t)n_elems * nv;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = __ldg(elems + e);
-        if (v < 0 || v >= n_nodes) continue;
-        const uint32_t lv = (uint32_t)(v - c_begin);
-        if (lv >= (uint32_t)n_cols) continue;
-        const int32_t t = (int32_t)(e / nv);
-        const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
-        const int32_t pos = __ldg(inc_ptr + lv) + atomicAdd(cursor + lv, 1);
-        inc[pos] = (j << 30) | (uint32_t)t;
-        if (emark) emark[t] = 1;
+    const int lane = threadIdx.x & 31;
+    const unsigned lower = (1u << lane) - 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane;
+    for (int64_t e0 = base; e0 < n_entries; e0 += stride) {
+        const int64_t e = e0 + lane;
+        int32_t key = -1;
+        if (e < n_entries) {
+            const int32_t v = __ldg(elems + e);
+            if (v >= 0 && v < n_nodes && (uint32_t)(v - c_begin) < (uint32_t)n_cols) key = v - c_begin;
+        }
+        const unsigned g = __match_any_sync(0xffffffffu, key);
+        // cursor starts at inc_ptr (one random-access array instead of two); the
+        // leader reserves the group's slots, members take base + rank
+        int32_t pos = 0;
+        if (key >= 0 && (g & lower) == 0) pos = atomicAdd(cursor + key, __popc(g));
+        pos = __shfl_sync(0xffffffffu, pos, __ffs(g) - 1) + __popc(g & lower);
+        if (key >= 0) {
+            const int32_t t = (int32_t)(e / nv);
+            const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
+            inc[pos] = (j << 30) | (uint32_t)t;
+            if (emark) emark[t] = 1;
+        }
     }
 }
 
@@ -148,7 +173,7 @@ k_inc_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage,
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_staged;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int2 s = __ldg(stage + q);
-        const int32_t pos = __ldg(inc_ptr + s.x) + atomicAdd(cursor + s.x, 1);
+        const int32_t pos = atomicAdd(cursor + s.x, 1);  // cursor starts at inc_ptr
         inc[pos] = (uint32_t)s.y;
         if (emark) emark[(uint32_t)s.y & 0x3FFFFFFFu] = 1;
     }
@@ -886,7 +911,9 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         nc, [cnt_c] __device__(int64_t i) { return (int64_t)cnt_c[i]; },
         mesh->inc_ptr.as<int32_t>(), ctx->scan_ws.p, s));
     count_launch(ctx);
-    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)nc + 1), s));
+    // fill cursors start at the segment offsets
+    FL_CUDA(cudaMemcpyAsync(cnt, mesh->inc_ptr.p, sizeof(int32_t) * ((size_t)nc + 1),
+                            cudaMemcpyDeviceToDevice, s));
     if (bucketed) {
         // bucket offsets = inc_ptr at the bucket boundaries
         int32_t* boff = bcnt + (kMaxBuckets + 1);
