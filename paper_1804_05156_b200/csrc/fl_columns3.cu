@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
 }
 
 template <int D, int L, bool PRE>
-__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 8 : 5) k_columns3(ColParams p) {
+__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3(ColParams p) {
     using C = V3<D, L>;
     constexpr int NV = D + 1;
     constexpr unsigned FULL = 0xffffffffu;
