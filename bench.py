@@ -313,7 +313,9 @@ def run_ours(args, rank: int, world: int):
     # ---- e2e through the C-ABI with host buffers (pinned) ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, (c0, c1) if world > 1 else None)
+        del res, dm  # release the device-resident run's buffers before the pipeline
+        ctx.synchronize()
+        e2e = run_e2e(args, cfg, torch, fl, _lib, L, C, dev, (c0, c1) if world > 1 else None)
         if world > 1:
             t = torch.tensor([e2e["ms_per_step"]], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -359,9 +361,16 @@ def run_ours(args, rank: int, world: int):
     return line
 
 
-def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, cols=None):
+def run_e2e(args, cfg, torch, fl, _lib, L, C, dev, cols=None):
+    """End to end through the C-ABI from pinned host memory, per step: upload the
+    mesh arrays (+ samples), assemble, synchronise for the sizes, copy every
+    output array back.  `--e2e-depth` fl_ctx objects (each with its own stream,
+    mesh and result) run consecutive steps as a pipeline -- step k's outputs
+    stream back while step k+1 uploads/computes -- the way a caller processing a
+    stream of meshes would use the API.  Throughput = steps / wall time."""
     m = cfg.mesh
     N, NT, d = m.num_nodes(), m.num_elems(), m.dim
+    depth = max(1, args.e2e_depth)
 
     def pinned(a):
         t = torch.empty(a.shape, dtype={np.float64: torch.float64, np.int32: torch.int32,
@@ -372,30 +381,35 @@ def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, cols=None):
     h_nodes, h_elems, h_flags = pinned(m.nodes), pinned(m.elems), pinned(m.bd_flags)
     f_arr = np.asarray(cfg.f) if isinstance(cfg.f, np.ndarray) else None
     h_f = pinned(f_arr) if f_arr is not None else None
-    # a separate fl_mesh fed from host memory every step
-    hmesh = C.c_void_p()
-    _lib.check(L.fl_mesh_create(ctx.handle, d, N, NT, h_nodes.data_ptr(), h_elems.data_ptr(),
-                                h_flags.data_ptr(), _lib.MEM_HOST, C.byref(hmesh)))
-    if cols is not None:
-        _lib.check(L.fl_mesh_set_columns(ctx.handle, hmesh, cols[0], cols[1]))
-    res = fl.AssemblyResult(ctx)
     ff, _k1 = fl.api._field_struct(cfg.f if f_arr is None else None, m, "load")
     if f_arr is not None:
         ff.kind, ff.mem, ff.samples, ff.n_samples = _lib.FIELD_SAMPLES, _lib.MEM_HOST, h_f.data_ptr(), f_arr.size
     fc, _k2 = fl.api._field_struct(cfg.coef, m, "coef")
     fd, _k3 = fl.api._field_struct(cfg.g_dirichlet, m, "dirichlet")
     fn, _k4 = fl.api._field_struct(cfg.g_neumann, m, "neumann")
-    outs = None
 
-    def e2e_step():
-        nonlocal outs
+    slots = []
+    for _ in range(depth):
+        ctx = fl.Context(dev)
+        hmesh = C.c_void_p()
+        _lib.check(L.fl_mesh_create(ctx.handle, d, N, NT, h_nodes.data_ptr(), h_elems.data_ptr(),
+                                    h_flags.data_ptr(), _lib.MEM_HOST, C.byref(hmesh)))
+        if cols is not None:
+            _lib.check(L.fl_mesh_set_columns(ctx.handle, hmesh, cols[0], cols[1]))
+        slots.append({"ctx": ctx, "mesh": hmesh, "res": fl.AssemblyResult(ctx), "outs": None})
+
+    def issue(sl):
+        ctx, hmesh = sl["ctx"], sl["mesh"]
         _lib.check(L.fl_mesh_set_nodes(ctx.handle, hmesh, h_nodes.data_ptr(), _lib.MEM_HOST))
         _lib.check(L.fl_mesh_set_elems(ctx.handle, hmesh, h_elems.data_ptr(), _lib.MEM_HOST))
         _lib.check(L.fl_mesh_set_flags(ctx.handle, hmesh, h_flags.data_ptr(), _lib.MEM_HOST))
         _lib.check(L.fl_assemble(ctx.handle, hmesh, C.byref(ff), C.byref(fc), C.byref(fd),
-                                 C.byref(fn), _lib.OUT_SYSTEM, res.handle))
+                                 C.byref(fn), _lib.OUT_SYSTEM | _lib.REPLAN, sl["res"].handle))
+
+    def drain(sl):
+        res = sl["res"]
         sz = res.sizes()
-        if outs is None:
+        if sl["outs"] is None:
             n, nf = sz.n, sz.n_free_cols  # this rank's columns (all of them at N=1)
             spec = [(_lib.A_COL_PTR, torch.int32, n + 1), (_lib.A_ROW_IDX, torch.int32, sz.nnz),
                     (_lib.A_VALUES, torch.float64, sz.nnz), (_lib.B, torch.float64, n),
@@ -404,29 +418,34 @@ def run_e2e(args, cfg, ctx, stream, torch, fl, _lib, L, C, dev, cols=None):
                     (_lib.AFF_COL_PTR, torch.int32, nf + 1),
                     (_lib.AFF_ROW_IDX, torch.int32, sz.nnz_ff),
                     (_lib.AFF_VALUES, torch.float64, sz.nnz_ff), (_lib.B_F, torch.float64, nf)]
-            outs = [(w, torch.empty(max(c, 1), dtype=t, pin_memory=True)) for w, t, c in spec]
-        for w, buf in outs:
+            sl["outs"] = [(w, torch.empty(max(c, 1), dtype=t, pin_memory=True)) for w, t, c in spec]
+        for w, buf in sl["outs"]:
             _lib.check(L.fl_result_copy(res.handle, w, buf.data_ptr(),
                                         buf.numel() * buf.element_size(), _lib.MEM_HOST))
         return sz
 
-    with torch.cuda.stream(stream):
-        for _ in range(max(1, args.warmup)):
-            sz = e2e_step()
-        times = []
-        for _ in range(max(1, min(args.steps, args.e2e_steps))):
-            ctx.synchronize()
-            t0 = time.perf_counter()
-            sz = e2e_step()
-            ctx.synchronize()
-            times.append(time.perf_counter() - t0)
-    L.fl_mesh_destroy(hmesh)
+    for sl in slots:  # warm-up (allocations, plan buffers, pinned outputs)
+        issue(sl)
+        drain(sl)
+    K = max(depth + 1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for k in range(K):
+        issue(slots[k % depth])
+        if k >= depth - 1:
+            drain(slots[(k - depth + 1) % depth])
+    for k in range(max(K - depth + 1, 0), K):
+        drain(slots[k % depth])
+    sec = (time.perf_counter() - t0) / K
     h2d = h_nodes.numel() * 8 + h_elems.numel() * 4 + h_flags.numel() + (f_arr.nbytes if f_arr is not None else 0)
-    d2h = sum(buf.numel() * buf.element_size() for _, buf in outs)
-    sec = float(np.mean(times))
+    d2h = sum(buf.numel() * buf.element_size() for _, buf in slots[0]["outs"])
+    for sl in slots:
+        L.fl_mesh_destroy(sl["mesh"])
+        del sl["res"]
     return {"value": NT / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3,
-            "timing": "wall clock per step, synchronised, host arrays in pinned memory"}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": K,
+            "timing": (f"wall clock over {K} steps, {depth}-deep pipeline of fl_ctx "
+                       "(upload | assemble | download overlap across consecutive steps), "
+                       "host arrays in pinned memory")}
 
 
 def main():
@@ -437,7 +456,8 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=12)
+    ap.add_argument("--e2e-depth", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per k_columns launch (from profiles/), echoed into roofline")

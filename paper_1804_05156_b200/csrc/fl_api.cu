@@ -119,6 +119,22 @@ static int rerun_general(fl_result* res, fl_result_ext* x) {
     fl_mesh* mesh = x->last_mesh;
     ColParams p = x->last;
     uint32_t* counters = res->counters.as<uint32_t>();
+    // the general kernel may need the plan's full output bound
+    const size_t cap = (size_t)std::max<int64_t>(mesh->nnz_bound, 1);
+    if (p.want_a) {
+        FL_TRY(res->arr[FL_A_ROW_IDX].ensure(sizeof(int32_t) * cap));
+        FL_TRY(res->arr[FL_A_VALUES].ensure(sizeof(double) * cap));
+        p.row_idx = res->arr[FL_A_ROW_IDX].as<int32_t>();
+        p.values = res->arr[FL_A_VALUES].as<double>();
+        p.cap_a = (int64_t)cap;
+    }
+    if (p.want_sys) {
+        FL_TRY(res->arr[FL_AFF_ROW_IDX].ensure(sizeof(int32_t) * cap));
+        FL_TRY(res->arr[FL_AFF_VALUES].ensure(sizeof(double) * cap));
+        p.ff_row_idx = res->arr[FL_AFF_ROW_IDX].as<int32_t>();
+        p.ff_values = res->arr[FL_AFF_VALUES].as<double>();
+        p.cap_ff = (int64_t)cap;
+    }
     FL_TRY(launch_inc_sort(ctx, mesh));
     FL_CUDA(cudaMemsetAsync(counters + CNT_TICKET, 0, sizeof(uint32_t), ctx->stream));
     FL_CUDA(cudaMemsetAsync(counters + CNT_ERR, 0, sizeof(uint32_t), ctx->stream));
@@ -337,6 +353,8 @@ FL_API int fl_mesh_plan(fl_ctx* ctx, fl_mesh* mesh) {
     mesh->nnz_bound = (int64_t)st[0];
     mesh->max_inc = (int32_t)st[1];
     mesh->planned = true;
+    mesh->ever_planned = true;
+    mesh->stats_stale = false;
     return FL_OK;
 }
 
@@ -397,13 +415,18 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[0], s));
     ctx->plan_timed = false;
     ctx->kernel_timed = false;
-    if (!mesh->planned && (what & (FL_OUT_STIFFNESS | FL_OUT_LOAD))) {
-        FL_TRY(fl_mesh_plan(ctx, mesh));
-        ctx->plan_timed = true;
-    } else if (replan && (what & (FL_OUT_STIFFNESS | FL_OUT_LOAD))) {
-        // same topology: rebuild asynchronously (the output bound is unchanged)
+    const bool need_plan = what & (FL_OUT_STIFFNESS | FL_OUT_LOAD);
+    if (need_plan && (replan || !mesh->planned) && mesh->ever_planned) {
+        // Rebuild asynchronously: allocation and kernel choice use the previous
+        // plan's bounds; fl_result_sizes refreshes the statistics and, should the
+        // new topology exceed them, re-runs the column pass on the general kernel.
         uint32_t* d_err = reinterpret_cast<uint32_t*>(mesh->stats.as<unsigned long long>() + 3);
         FL_TRY(launch_plan_kernels(ctx, mesh, d_err));
+        mesh->planned = true;
+        mesh->stats_stale = true;
+        ctx->plan_timed = true;
+    } else if (need_plan && !mesh->planned) {
+        FL_TRY(fl_mesh_plan(ctx, mesh));
         ctx->plan_timed = true;
     }
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
@@ -430,7 +453,14 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
 
     // outputs (column-indexed ones hold the owned range only)
     const size_t n1 = (size_t)N + 1, nc1 = (size_t)NC + 1;
-    const size_t cap = (size_t)std::max<int64_t>(mesh->nnz_bound, 1);
+    // Output capacity.  The tiled / register kernels keep at most 12 (2-D) /
+    // 24 (3-D) distinct rows per column (else they flag the general kernel,
+    // which re-sizes to the plan's bound in rerun_general): size for that.
+    const char* kern = std::getenv("FL_KERNEL");
+    const char kk = kern ? kern[0] : '0';
+    const int64_t fast_rows = mesh->dim == 2 ? 12 : 24;
+    const int64_t bound = std::max<int64_t>(mesh->nnz_bound, 1);
+    const size_t cap = (size_t)(kk == '1' ? bound : std::min<int64_t>(bound, fast_rows * std::max(NC, 1)));
     uint32_t* counters = res->counters.as<uint32_t>();
     FL_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * CNT_WORDS, s));
     if (want_a) {
@@ -522,8 +552,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             // element records + v3 (register-centric) by default; v2 (tiled)
             // carries the Dirichlet lift; v1 (general) is the fallback.
             // FL_KERNEL=1|2|3 forces one (3 = v3 with in-kernel geometry).
-            const char* kern = std::getenv("FL_KERNEL");
-            const char k = kern ? kern[0] : '0';
+            const char k = kk;
             if (k == '1') {
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
@@ -552,6 +581,11 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
                                 cudaMemcpyDeviceToHost, s));
         int32_t* hn = reinterpret_cast<int32_t*>(h + CNT_WORDS);
         hn[0] = hn[1] = hn[2] = hn[3] = hn[4] = 0;
+        fl_mesh* lm = x->last_valid ? x->last_mesh : nullptr;
+        unsigned long long* hst = reinterpret_cast<unsigned long long*>(h + CNT_WORDS + 16);
+        if (lm && lm->stats_stale)
+            FL_CUDA(cudaMemcpyAsync(hst, lm->stats.p, sizeof(unsigned long long) * 4,
+                                    cudaMemcpyDeviceToHost, s));
         const bool sharded_sys = (res->what & FL_OUT_SYSTEM) && res->n != res->m;
         if (sharded_sys) {  // free nodes before / through the range
             const int32_t* fr = res->fidx.as<int32_t>() + (size_t)res->m + 1;
@@ -564,7 +598,18 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
             FL_CUDA(cudaMemcpyAsync(&hn[0], res->arr[FL_A_COL_PTR].as<int32_t>() + res->n,
                                     sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         FL_CUDA(cudaStreamSynchronize(s));
-        if ((h[CNT_ERR] & DERR_V2_OVERFLOW) && x->last_valid) {
+        bool replanned = false;
+        if (lm && lm->stats_stale) {  // an asynchronous re-plan ran with the old bounds
+            lm->nnz_bound = (int64_t)hst[0];
+            lm->max_inc = (int32_t)hst[1];
+            lm->stats_stale = false;
+            replanned = true;
+            if ((uint32_t)(hst[3] & 0xFFFFFFFFull) & DERR_INDEX) h[CNT_ERR] |= DERR_INDEX;
+        }
+        // a new topology that outgrew the old bounds: redo the column pass sized
+        // by the fresh plan (general kernel)
+        if (((h[CNT_ERR] & DERR_V2_OVERFLOW) || (replanned && (h[CNT_ERR] & DERR_CAPACITY))) &&
+            x->last_valid && !(h[CNT_ERR] & DERR_INDEX)) {
             FL_TRY(rerun_general(res, x));
             FL_CUDA(cudaMemcpyAsync(h, res->counters.p, sizeof(uint32_t) * CNT_WORDS,
                                     cudaMemcpyDeviceToHost, s));

@@ -134,3 +134,49 @@ def test_bucketed_plan_matches_golden(tag, world, ctx, monkeypatch):
     np.testing.assert_array_equal(full.row_idx, g["a_row_idx"])
     assert _bits(full.values) == _bits(g["a_values"])
     assert _bits(np.concatenate([r.vector(_lib.B) for _, r, _ in parts])) == _bits(g["b_1"])
+
+
+def test_async_replan_after_new_connectivity(ctx):
+    """fl_mesh_set_elems + FL_REPLAN re-plans asynchronously with the old bounds;
+    fl_result_sizes refreshes them (and re-runs the column pass if exceeded)."""
+    import ctypes as C
+    from paper_1804_05156_b200 import api
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "square8_jit.npz"))
+    m = _mesh(g)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(m.num_nodes()).astype(np.int32)   # node k -> perm[k]
+    inv = np.argsort(perm)
+    elems_b = perm[m.elems].astype(np.int32)
+    nodes_b = np.ascontiguousarray(m.nodes.reshape(-1, 2)[inv])
+    mb = Mesh(2, nodes_b, elems_b, g["flags"])
+    want = fl.assemble_blockwise(mb, ctx=ctx)
+    L = _lib.lib()
+    dm = m.device(ctx)
+    dm.plan()
+    _lib.check(L.fl_mesh_set_elems(ctx.handle, dm.handle, elems_b.ctypes.data, _lib.MEM_HOST))
+    _lib.check(L.fl_mesh_set_nodes(ctx.handle, dm.handle, nodes_b.ctypes.data, _lib.MEM_HOST))
+    res = api.run(mb, _lib.OUT_STIFFNESS | _lib.REPLAN, ctx=ctx, device_mesh=dm)
+    got = res.matrix()
+    np.testing.assert_array_equal(got.col_ptr, want.col_ptr)
+    np.testing.assert_array_equal(got.row_idx, want.row_idx)
+    assert _bits(got.values) == _bits(want.values)
+    # a topology with a higher-valence node than the old bounds allow (fan of 40)
+    k = 40
+    ang = 2 * np.pi * np.arange(k) / k
+    fan_nodes = np.vstack([[0.0, 0.0], np.stack([np.cos(ang), np.sin(ang)], 1)])
+    fan_elems = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)], dtype=np.int32)
+    small = Mesh(2, fan_nodes, np.array([[1 + i, 1 + (i + 1) % k, 1 + (i + 2) % k]
+                                         for i in range(k)], dtype=np.int32))
+    from tests.meshes import fix_orientation
+    small = Mesh(2, fan_nodes, fix_orientation(2, fan_nodes, small.elems))
+    fan = Mesh(2, fan_nodes, fix_orientation(2, fan_nodes, fan_elems))
+    want = fl.assemble_blockwise(fan, ctx=ctx)
+    dm2 = small.device(ctx)
+    dm2.plan()
+    fe = np.ascontiguousarray(fan.elems, dtype=np.int32)
+    _lib.check(L.fl_mesh_set_elems(ctx.handle, dm2.handle, fe.ctypes.data, _lib.MEM_HOST))
+    res = api.run(fan, _lib.OUT_STIFFNESS | _lib.REPLAN, ctx=ctx, device_mesh=dm2)
+    got = res.matrix()
+    np.testing.assert_array_equal(got.col_ptr, want.col_ptr)
+    np.testing.assert_array_equal(got.row_idx, want.row_idx)
+    assert _bits(got.values) == _bits(want.values)
