@@ -75,7 +75,7 @@ __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* 
 constexpr int kElemThreads = 128;
 
 template <int D>
-__global__ void __launch_bounds__(kElemThreads) k_elem_records(ColParams p) {
+__global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
     constexpr int NV = D + 1;
     constexpr int W = 8 + 1;  // int4 words per element in smem (+1: no bank conflicts)
     __shared__ int4 stage[kElemThreads * W];
