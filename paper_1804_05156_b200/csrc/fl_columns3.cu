@@ -8,7 +8,7 @@
 //      incidence in (j, t) order -- the order in which the reference's
 //      blockwise triplets reach column c (assembly.hpp:286-298 after the stable
 //      passes sparse.hpp:79-89);
-//   2. each lane reads its incidence from the 128-byte element record (k_elem_records:
+//   2. each lane reads its incidence's row of the element record (k_elem_records,
 //      s_ij for i = 0..d, the load share, the vertices; FMA-free, exact
 //      division) -- or, with FL_KERNEL=3, computes them itself (fl_geometry.cuh);
 //   3. b = 0.0 + shares in lane order (system.hpp:114-118) and the diagonal
@@ -77,7 +77,10 @@ constexpr int kElemThreads = 128;
 template <int D>
 __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
     constexpr int NV = D + 1;
-    constexpr int W = 8 + 1;  // int4 words per element in smem (+1: no bank conflicts)
+    // per element: D == 3: the full local matrix, row-major (8 int4) + 4 load
+    // shares (2 int4); D == 2: rows {s_0j, s_1j, s_2j, load_j} (6 int4)
+    constexpr int WS = D == 3 ? 8 : 6, WL = D == 3 ? 2 : 0;
+    constexpr int W = WS + WL + 1;  // +1: no bank conflicts
     __shared__ int4 stage[kElemThreads * W];
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
@@ -122,30 +125,32 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
                 if (p.want_b) ec.load_all((int32_t)t, meas, p.f, Lj);
                 else Lj[0] = Lj[1] = Lj[2] = Lj[3] = 0.0;
             }
-            // one 128-byte record per element: the upper triangle of the local
-            // matrix (s_ij == s_ji), the d+1 load shares, the vertex ids
-            double rec[16];
-            int k = 0;
-#pragma unroll
-            for (int a = 0; a < NV; ++a)
-#pragma unroll
-                for (int b = a; b < NV; ++b) rec[k++] = S[a][b];
-#pragma unroll
-            for (int a = 0; a < NV; ++a) rec[k++] = Lj[a];
-            for (; k < 14; ++k) rec[k] = 0.0;
+            // records: row j of the local matrix (= column j, s_ij == s_ji) is one
+            // 32-byte line the column kernel reads with a single 256-bit load
             int4* st = stage + threadIdx.x * W;
 #pragma unroll
-            for (int q = 0; q < 7; ++q) {
-                double2 w = make_double2(rec[2 * q], rec[2 * q + 1]);
-                st[q] = *reinterpret_cast<int4*>(&w);
+            for (int j = 0; j < NV; ++j) {
+                double2 w0 = make_double2(S[j][0], S[j][1]);
+                double2 w1 = make_double2(S[j][2], D == 3 ? S[j][3] : Lj[j]);
+                st[2 * j] = *reinterpret_cast<int4*>(&w0);
+                st[2 * j + 1] = *reinterpret_cast<int4*>(&w1);
             }
-            st[7] = make_int4(V[0], V[1], V[2], D == 3 ? V[3] : 0);
+            if constexpr (D == 3) {
+                double2 l01 = make_double2(Lj[0], Lj[1]), l23 = make_double2(Lj[2], Lj[3]);
+                st[WS] = *reinterpret_cast<int4*>(&l01);
+                st[WS + 1] = *reinterpret_cast<int4*>(&l23);
+            }
         }
         __syncthreads();
         // coalesced write-out of the block's contiguous records
         const int64_t n = min((int64_t)kElemThreads, p.n_elems - t0);
-        int4* out = reinterpret_cast<int4*>(p.srec) + t0 * 8;
-        for (int q = threadIdx.x; q < n * 8; q += kElemThreads) out[q] = stage[(q >> 3) * W + (q & 7)];
+        int4* out = reinterpret_cast<int4*>(p.srec) + t0 * WS;
+        for (int q = threadIdx.x; q < n * WS; q += kElemThreads) out[q] = stage[(q / WS) * W + q % WS];
+        if constexpr (WL > 0) {
+            int4* outl = reinterpret_cast<int4*>(p.lrec) + t0 * WL;
+            for (int q = threadIdx.x; q < n * WL; q += kElemThreads)
+                outl[q] = stage[(q / WL) * W + WS + q % WL];
+        }
         __syncthreads();
     }
 }
@@ -227,19 +232,28 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 s[i] = 0.0;
             }
             if (valid && PRE) {
-                // the element's 128-byte record: s_ij at the upper-triangle slot of
-                // (min(i,j), max(i,j)), then the load shares, then the vertex ids
-                const double* rec = p.srec + (size_t)t * 16;
-                constexpr uint64_t TRI = D == 3 ? 0x9863875265413210ull   // slot of (i, j): 4 bits
-                                                : 0x0000054204310210ull;  // at 4 * (4j + i)
+                // row j of the element's local matrix: one 256-bit load; the load
+                // share (3-D) and the vertex ids from their own arrays
+                const double* row = p.srec + ((size_t)t * NV + j) * 4;
+                double q0, q1, q2, q3;
+                asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                    : "=d"(q0), "=d"(q1), "=d"(q2), "=d"(q3) : "l"(row));
+                s[0] = q0;
+                s[1] = q1;
+                s[2] = q2;
+                if constexpr (D == 3) {
+                    s[3] = q3;
+                    l = __ldg(p.lrec + (size_t)t * 4 + j);
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
+                    R[0] = e.x;
+                    R[1] = e.y;
+                    R[2] = e.z;
+                    R[3] = e.w;
+                } else {
+                    l = q3;
 #pragma unroll
-                for (int i = 0; i < NV; ++i) s[i] = __ldg(rec + ((TRI >> (4 * (4 * j + i))) & 15));
-                l = __ldg(rec + (D == 3 ? 10 : 6) + j);
-                const int4 e = __ldg(reinterpret_cast<const int4*>(rec) + 7);
-                R[0] = e.x;
-                R[1] = e.y;
-                R[2] = e.z;
-                if constexpr (D == 3) R[3] = e.w;
+                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t * NV + i);
+                }
             } else if (valid) {
                 if constexpr (D == 3) {
                     const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
@@ -494,9 +508,10 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     }
     if constexpr (PRE) {
         const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
-        FL_TRY(res->erec[0].ensure((size_t)128 * ne));
+        FL_TRY(res->erec[0].ensure(sizeof(double) * 4 * (D + 1) * ne));
+        if (D == 3) FL_TRY(res->erec[1].ensure(sizeof(double) * 4 * ne));
         p.srec = res->erec[0].as<double>();
-        p.lrec = nullptr;
+        p.lrec = D == 3 ? res->erec[1].as<double>() : nullptr;
         if (p.n_elems > 0) {
             const int g = std::min(div_up(p.n_elems, kElemThreads), ctx->sm_count * 16);
             k_elem_records<D><<<g, kElemThreads, 0, ctx->stream>>>(p);

@@ -53,10 +53,11 @@ struct ColParams {
     int32_t* tile_off;   // [2][n_tiles + 1]: exclusive scans of tile_tot
     int32_t* colcnt_a;   // [N] in-tile inclusive count after column c
     int32_t* colcnt_f;   // [N] same for A(free, free) (indexed by column c)
-    // element-first records (k_elem_records): one 128-byte record per element at
-    // srec + 16t: upper triangle of the local matrix, d+1 load shares, vertex ids
+    // element-first records (k_elem_records): srec row (t, j) at 4(t(d+1) + j) =
+    // {s_0j, s_1j, s_2j, s_3j} (3-D) / {s_0j, s_1j, s_2j, load_j} (2-D); lrec
+    // [t][j] = load share (3-D)
     double* srec;
-    double* lrec;  // unused
+    double* lrec;
     const uint8_t* emark;  // sharded: records only for elements touching owned columns
 };
 
