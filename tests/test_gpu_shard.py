@@ -180,3 +180,21 @@ def test_async_replan_after_new_connectivity(ctx):
     np.testing.assert_array_equal(got.col_ptr, want.col_ptr)
     np.testing.assert_array_equal(got.row_idx, want.row_idx)
     assert _bits(got.values) == _bits(want.values)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_result_counts_async_matches_sizes(world, ctx):
+    """fl_result_counts_async (the payload of the NCCL nnz-offset exchange)."""
+    import ctypes as C
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cube3_mixed_jit.npz"))
+    m = _mesh(g)
+    for r in range(world):
+        sa = ShardedAssembler(m, r, world, ctx=ctx)
+        res = sa.assemble(_lib.OUT_SYSTEM, f=1.0, g_dirichlet=0.0)
+        s = res.sizes()
+        import torch
+        out = torch.zeros(4, dtype=torch.int64, device="cuda")
+        ctx.synchronize()
+        _lib.check(_lib.lib().fl_result_counts_async(res.handle, C.c_void_p(out.data_ptr())))
+        ctx.synchronize()
+        assert out.cpu().tolist() == [s.n, s.n_free_cols, s.nnz, s.nnz_ff]
