@@ -41,6 +41,9 @@ SIGNATURES = {
     "fl_mesh_plan": (C.c_int, [_vp, _vp]),
     "fl_mesh_set_columns": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32]),
     "fl_result_counts_async": (C.c_int, [_vp, _vp]),
+    "fl_boundary_faces": (C.c_int, [_vp, _vp, _vp]),
+    "fl_boundary_faces_copy": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
+    "fl_mesh_set_boundary_flags": (C.c_int, [_vp, _vp, _vp, C.c_int8, C.c_int]),
     "fl_mesh_destroy": (C.c_int, [_vp]),
     "fl_result_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "fl_result_destroy": (C.c_int, [_vp]),

@@ -268,6 +268,7 @@ FL_API int fl_mesh_create(fl_ctx* ctx, int dim, int32_t n_nodes, int32_t n_elems
 
 FL_API int fl_mesh_set_nodes(fl_ctx* ctx, fl_mesh* mesh, const double* nodes, int mem) {
     if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    mesh->n_bfaces = -1;
     return copy_in(ctx, mesh->nodes, nodes, sizeof(double) * (size_t)mesh->n_nodes * mesh->dim, mem);
 }
 
@@ -283,6 +284,7 @@ FL_API int fl_mesh_set_flags(fl_ctx* ctx, fl_mesh* mesh, const int8_t* bd_flags,
 
 FL_API int fl_mesh_set_elems(fl_ctx* ctx, fl_mesh* mesh, const int32_t* elems, int mem) {
     if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    mesh->n_bfaces = -1;
     mesh->planned = false;
     return copy_in(ctx, mesh->elems, elems, sizeof(int32_t) * (size_t)mesh->n_elems * (mesh->dim + 1),
                    mem);
@@ -298,6 +300,41 @@ FL_API int fl_mesh_set_columns(fl_ctx* ctx, fl_mesh* mesh, int32_t col_begin, in
     return FL_OK;
 }
 
+// ---- boundary faces (set_boundary_flags, mesh.hpp:251-304) ---------------------------
+FL_API int fl_boundary_faces(fl_ctx* ctx, fl_mesh* mesh, int64_t* n_faces) {
+    if (!ctx || !mesh || !n_faces) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (mesh->col_begin != 0 || mesh->col_end != mesh->n_nodes)
+        return set_error(FL_ERR_ARGUMENT, "boundary faces need the whole mesh (no column range)");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    if (!mesh->planned || mesh->stats_stale) FL_TRY(fl_mesh_plan(ctx, mesh));
+    return launch_boundary_faces(ctx, mesh, n_faces);
+}
+
+FL_API int fl_boundary_faces_copy(fl_ctx* ctx, fl_mesh* mesh, int32_t* faces, double* centroids,
+                                  int mem) {
+    if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (mesh->n_bfaces < 0) return set_error(FL_ERR_ARGUMENT, "call fl_boundary_faces first");
+    const size_t nb = (size_t)mesh->n_bfaces;
+    const cudaMemcpyKind kind = mem == FL_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (faces && nb) FL_CUDA(cudaMemcpyAsync(faces, mesh->bfaces.p, sizeof(int32_t) * 2 * nb, kind, ctx->stream));
+    if (centroids && nb)
+        FL_CUDA(cudaMemcpyAsync(centroids, mesh->bcent.p, sizeof(double) * 3 * nb, kind, ctx->stream));
+    if (mem != FL_MEM_DEVICE) FL_CUDA(cudaStreamSynchronize(ctx->stream));
+    return FL_OK;
+}
+
+FL_API int fl_mesh_set_boundary_flags(fl_ctx* ctx, fl_mesh* mesh, const int8_t* face_flags,
+                                      int8_t fill, int mem) {
+    if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (mesh->n_bfaces < 0) return set_error(FL_ERR_ARGUMENT, "call fl_boundary_faces first");
+    const int8_t* vals = nullptr;
+    if (face_flags) {
+        FL_TRY(copy_in(ctx, mesh->bstage, face_flags, (size_t)mesh->n_bfaces, mem));
+        vals = mesh->bstage.as<int8_t>();
+    }
+    return launch_boundary_scatter(ctx, mesh, vals, fill);
+}
+
 FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     if (!mesh) return FL_OK;
     if (mesh->ctx) cudaStreamSynchronize(mesh->ctx->stream);
@@ -308,6 +345,10 @@ FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     mesh->inc.release();
     mesh->cursor.release();
     mesh->emark.release();
+    mesh->bmark.release();
+    mesh->bpos.release();
+    mesh->bfaces.release();
+    mesh->bcent.release();
     mesh->bstage.release();
     mesh->bcnt.release();
     mesh->stats.release();

@@ -81,6 +81,8 @@ int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t c
 int finish_staging(fl_ctx* ctx, ColParams& p, int tc);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
 int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out);
+int launch_boundary_faces(fl_ctx* ctx, fl_mesh* mesh, int64_t* n_faces);
+int launch_boundary_scatter(fl_ctx* ctx, fl_mesh* mesh, const int8_t* values, int8_t fill);
 size_t column_smem_bytes();
 int column_tile_width();
 
