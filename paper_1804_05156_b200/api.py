@@ -12,6 +12,7 @@ Every function calls libfemlite_b200.so; there is no host fallback.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 import enum
 from dataclasses import dataclass, field
 from typing import Optional
@@ -209,6 +210,8 @@ class AssemblyResult:
                                  s.n_dir_faces, s.n_neu_faces)
 
     def __del__(self):
+        if sys.is_finalizing():  # the CUDA runtime may already be gone; the OS reclaims
+            return
         try:
             if self._h:
                 _lib.lib().fl_result_destroy(self._h)

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import sys
 
 from . import _lib
 
@@ -53,6 +54,8 @@ class Context:
             self._h = C.c_void_p()
 
     def __del__(self):
+        if sys.is_finalizing():  # the CUDA runtime may already be gone; the OS reclaims
+            return
         try:
             self.close()
         except Exception:

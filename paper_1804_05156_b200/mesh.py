@@ -14,6 +14,7 @@ of mesh.hpp:251-405 that are checked against the reference in tests.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 import enum
 
 import numpy as np
@@ -103,6 +104,8 @@ class DeviceMesh:
         _lib.check(_lib.lib().fl_mesh_validate(self.ctx.handle, self._h), "fl_mesh_validate")
 
     def __del__(self):
+        if sys.is_finalizing():  # the CUDA runtime may already be gone; the OS reclaims
+            return
         try:
             if self._h:
                 _lib.lib().fl_mesh_destroy(self._h)
