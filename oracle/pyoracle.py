@@ -397,3 +397,41 @@ def ref_time_system(dim, nodes, elems, flags, f_kind, f_value=0.0, coef=None, re
                              C.c_double(f_value), _p(coef, _f64p), C.c_int(reps), _p(secs, _f64p),
                              C.byref(nnz), C.byref(nnz_ff)), "ref")
     return secs, nnz.value, nnz_ff.value
+
+
+def ref_matvec(a: Csc, x):
+    """The reference's matvec (sparse.hpp:129-141)."""
+    L = lib("ref")
+    x = _arr_f64(x)
+    y = np.zeros(a.m, dtype=np.float64)
+    _check(L.ref_matvec(C.c_int32(a.m), C.c_int32(a.n), _p(_arr_i32(a.col_ptr), _i32p),
+                        _p(_arr_i32(a.row_idx), _i32p), _p(_arr_f64(a.values), _f64p), _p(x, _f64p),
+                        _p(y, _f64p)), "ref")
+    return y
+
+
+def ref_cg_solve(a: Csc, b, rel_tol=1e-10, max_iter=0, precond=2):
+    """The reference's cg_solve (solver.hpp:63-136): (x, iterations, relres, converged)."""
+    L = lib("ref")
+    b = _arr_f64(b)
+    x = np.zeros(a.n, dtype=np.float64)
+    it, rr, cv = C.c_int64(), C.c_double(), C.c_int32()
+    cp, ri, va = _arr_i32(a.col_ptr), _arr_i32(a.row_idx), _arr_f64(a.values)
+    _check(L.ref_cg_solve(C.c_int32(a.n), _p(cp, _i32p), _p(ri, _i32p), _p(va, _f64p), _p(b, _f64p),
+                          C.c_double(rel_tol), C.c_int64(max_iter), C.c_int(precond), _p(x, _f64p),
+                          C.byref(it), C.byref(rr), C.byref(cv)), "ref")
+    return x, it.value, rr.value, bool(cv.value)
+
+
+def ref_solve_poisson(dim, nodes, elems, flags, f_kind, f_value, g_kind, g_value, rel_tol=1e-10):
+    """The reference's solve_poisson on a Dirichlet mesh: (u, iterations, relres, seconds)."""
+    L = lib("ref")
+    nodes, elems, flags = _arr_f64(nodes), _arr_i32(elems), _arr_i8(flags)
+    u = np.zeros(nodes.shape[0], dtype=np.float64)
+    it, rr, sec = C.c_int64(), C.c_double(), C.c_double()
+    _check(L.ref_solve_poisson(C.c_int(dim), C.c_int32(nodes.shape[0]), C.c_int32(elems.shape[0]),
+                               _p(nodes, _f64p), _p(elems, _i32p), _p(flags, _i8p), C.c_int(f_kind),
+                               C.c_double(f_value), C.c_int(g_kind), C.c_double(g_value),
+                               C.c_double(rel_tol), _p(u, _f64p), C.byref(it), C.byref(rr),
+                               C.byref(sec)), "ref")
+    return u, it.value, rr.value, sec.value

@@ -350,4 +350,54 @@ int ref_time_system(int dim, int32_t n_nodes, int32_t n_elems, const double* nod
     });
 }
 
+// sparse.hpp:129-141
+int ref_matvec(int32_t m, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
+               const double* values, const double* x, double* y_out) {
+    return guarded([&] {
+        const CscMatrix a = import_csc(m, n, col_ptr, row_idx, values);
+        const std::vector<double> y = matvec(a, std::span<const double>(x, std::size_t(n)));
+        std::memcpy(y_out, y.data(), sizeof(double) * y.size());
+    });
+}
+
+// solver.hpp:63-136; precond 0 none, 1 jacobi, 2 auto
+int ref_cg_solve(int32_t n, const int32_t* col_ptr, const int32_t* row_idx, const double* values,
+                 const double* b, double rel_tol, int64_t max_iter, int precond, double* x_out,
+                 int64_t* iterations, double* relres, int32_t* converged) {
+    return guarded([&] {
+        const CscMatrix a = import_csc(n, n, col_ptr, row_idx, values);
+        SolveOptions o;
+        o.rel_tol = rel_tol;
+        o.max_iter = static_cast<index_t>(max_iter);
+        o.preconditioner = precond == 0 ? Preconditioner::none
+                         : precond == 1 ? Preconditioner::jacobi : Preconditioner::auto_select;
+        const CgResult r = cg_solve(a, std::span<const double>(b, std::size_t(n)), o);
+        std::memcpy(x_out, r.x.data(), sizeof(double) * r.x.size());
+        *iterations = r.iterations;
+        *relres = r.relres;
+        *converged = r.converged ? 1 : 0;
+    });
+}
+
+// solver.hpp:223-247 (Dirichlet meshes): u, iterations, relres; wall seconds
+int ref_solve_poisson(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                      const int32_t* elems, const int8_t* flags, int f_kind, double f_value,
+                      int g_kind, double g_value, double rel_tol, double* u_out,
+                      int64_t* iterations, double* relres, double* seconds) {
+    return guarded([&] {
+        const Mesh m = mesh_from(dim, n_nodes, n_elems, nodes, elems, flags);
+        PoissonProblem pb;
+        pb.f = make_field(f_kind, f_value, nullptr, nullptr);
+        pb.g_dirichlet = make_field(g_kind, g_value, nullptr, nullptr);
+        SolveOptions o;
+        o.rel_tol = rel_tol;
+        const auto t0 = std::chrono::steady_clock::now();
+        const Solution sol = solve_poisson(m, pb, o);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::memcpy(u_out, sol.u.data(), sizeof(double) * sol.u.size());
+        *iterations = sol.iterations;
+        *relres = sol.final_relres;
+    });
+}
+
 } // extern "C"

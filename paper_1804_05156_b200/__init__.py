@@ -8,14 +8,17 @@ Public API mirrors femlite (/root/reference/proj/include/femlite/):
     assemble_load, partition_boundary, apply_neumann,
     BoundaryPartition, DirichletSystem                                  system.hpp
     assemble_system / poisson_system  (solve_poisson's pre-solve path,  solver.hpp:226-242)
+    matvec, cg_solve, solve_poisson (§8(f) row 2)                       sparse.hpp, solver.hpp
+    boundary.set_boundary_flags (GPU face matching, §8(f) row 1)        mesh.hpp:251-304
     ErrorCode, Error                                                    error.hpp
 
 All compute runs in libfemlite_b200.so (hand-written sm_100a kernels behind
 the C-ABI of include/femlite_b200.h); importing does not touch the GPU.
 """
-from .api import (AssemblyResult, AssemblyStrategy, BoundaryPartition, CscMatrix, DirichletSystem,
-                  PoissonSystem, assemble, assemble_blockwise, assemble_load, assemble_system,
-                  apply_neumann, partition_boundary, poisson_system, run, submatrix)
+from .api import (AssemblyResult, AssemblyStrategy, BoundaryPartition, CgResult, CscMatrix,
+                  DirichletSystem, PoissonSystem, Solution, assemble, assemble_blockwise,
+                  assemble_load, assemble_system, apply_neumann, cg_solve, matvec, partition_boundary,
+                  poisson_system, run, solve_poisson, submatrix)
 from .context import Context
 from .errors import Error, ErrorCode
 from .mesh import (Mesh, MeshShape, boundary_face_mask, classifier_dirichlet, classifier_lshape,
@@ -23,10 +26,11 @@ from .mesh import (Mesh, MeshShape, boundary_face_mask, classifier_dirichlet, cl
                    set_boundary_flags)
 
 __all__ = [
-    "AssemblyResult", "AssemblyStrategy", "BoundaryPartition", "Context", "CscMatrix",
+    "AssemblyResult", "AssemblyStrategy", "BoundaryPartition", "CgResult", "Context", "CscMatrix",
     "DirichletSystem", "Error", "ErrorCode", "Mesh", "MeshShape", "PoissonSystem", "assemble",
     "assemble_blockwise", "assemble_load", "assemble_system", "apply_neumann",
     "boundary_face_mask", "classifier_dirichlet", "classifier_lshape", "classifier_mixed",
     "classifier_neumann", "flag_generated", "generate_mesh", "make_mesh", "partition_boundary",
-    "poisson_system", "run", "set_boundary_flags", "submatrix",
+    "poisson_system", "run", "set_boundary_flags", "submatrix", "cg_solve", "matvec", "solve_poisson",
+    "Solution",
 ]

@@ -42,6 +42,9 @@ SIGNATURES = {
     "fl_mesh_set_columns": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32]),
     "fl_result_counts_async": (C.c_int, [_vp, _vp]),
     "fl_boundary_faces": (C.c_int, [_vp, _vp, _vp]),
+    "fl_cg_solve": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp]),
+    "fl_solve_system": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "fl_matvec": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_int]),
     "fl_boundary_faces_copy": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
     "fl_mesh_set_boundary_flags": (C.c_int, [_vp, _vp, _vp, C.c_int8, C.c_int]),
     "fl_mesh_destroy": (C.c_int, [_vp]),
@@ -67,6 +70,11 @@ SIGNATURES = {
 class Field(C.Structure):
     _fields_ = [("kind", C.c_int32), ("mem", C.c_int32), ("value", C.c_double),
                 ("samples", _vp), ("n_samples", C.c_int64)]
+
+
+class CgOptions(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("max_iter", C.c_int64), ("preconditioner", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 class Sizes(C.Structure):

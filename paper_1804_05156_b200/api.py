@@ -12,8 +12,8 @@ Every function calls libfemlite_b200.so; there is no host fallback.
 from __future__ import annotations
 
 import ctypes as C
-import sys
 import enum
+import sys
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -334,3 +334,82 @@ def submatrix(a: CscMatrix, rows, cols, ctx: Optional[Context] = None) -> CscMat
                      res.array(_lib.A_COL_PTR, np.int32, cols.size + 1),
                      res.array(_lib.A_ROW_IDX, np.int32, s.nnz),
                      res.array(_lib.A_VALUES, np.float64, s.nnz))
+
+
+# ---------------------------------------------------------------------------
+# the solve after the path
+# ---------------------------------------------------------------------------
+_PRECOND = {"none": 0, "jacobi": 1, "auto": 2, "auto_select": 2}
+
+
+@dataclass
+class CgResult:  # solver.hpp:34-39
+    x: np.ndarray
+    iterations: int
+    relres: float
+    converged: bool
+
+
+@dataclass
+class Solution:  # solver.hpp:179-184
+    u: np.ndarray
+    iterations: int
+    final_relres: float
+    partition: BoundaryPartition
+
+
+def _cg_options(rel_tol, max_iter, preconditioner):
+    o = _lib.CgOptions()
+    o.rel_tol, o.max_iter = float(rel_tol), int(max_iter)
+    o.preconditioner = _PRECOND[preconditioner] if isinstance(preconditioner, str) else int(preconditioner)
+    return o
+
+
+def matvec(a: CscMatrix, x, ctx: Optional[Context] = None) -> np.ndarray:
+    """sparse.hpp:129: y = A x on the GPU, bitwise the reference's order."""
+    ctx = ctx or Context.default()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.shape[0] != a.n:
+        raise Error(ErrorCode.shape_mismatch, "matvec: vector length mismatch")
+    y = np.empty(a.m, dtype=np.float64)
+    cp = np.ascontiguousarray(a.col_ptr, dtype=np.int32)
+    ri = np.ascontiguousarray(a.row_idx, dtype=np.int32)
+    va = np.ascontiguousarray(a.values, dtype=np.float64)
+    _lib.check(_lib.lib().fl_matvec(ctx.handle, a.m, a.n, cp.ctypes.data, ri.ctypes.data, va.ctypes.data,
+                                    x.ctypes.data, y.ctypes.data, _lib.MEM_HOST), "fl_matvec")
+    return y
+
+
+def cg_solve(a: CscMatrix, b, rel_tol: float = 1e-10, max_iter: int = 0, preconditioner="auto",
+             ctx: Optional[Context] = None) -> CgResult:
+    """solver.hpp:63: preconditioned CG on the GPU (x0 = 0; best iterate on the cap)."""
+    ctx = ctx or Context.default()
+    if a.m != a.n:
+        raise Error(ErrorCode.shape_mismatch, "cg_solve: matrix not square")
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.shape[0] != a.n:
+        raise Error(ErrorCode.shape_mismatch, "cg_solve: vector length mismatch")
+    x = np.empty(a.n, dtype=np.float64)
+    it, rr, cv = C.c_int64(), C.c_double(), C.c_int32()
+    cp = np.ascontiguousarray(a.col_ptr, dtype=np.int32)
+    ri = np.ascontiguousarray(a.row_idx, dtype=np.int32)
+    va = np.ascontiguousarray(a.values, dtype=np.float64)
+    o = _cg_options(rel_tol, max_iter, preconditioner)
+    _lib.check(_lib.lib().fl_cg_solve(ctx.handle, a.n, cp.ctypes.data, ri.ctypes.data, va.ctypes.data,
+                                      b.ctypes.data, _lib.MEM_HOST, C.byref(o), x.ctypes.data,
+                                      C.byref(it), C.byref(rr), C.byref(cv)), "fl_cg_solve")
+    return CgResult(x, it.value, rr.value, bool(cv.value))
+
+
+def solve_poisson(mesh: Mesh, f, g_dirichlet, g_neumann=None, coef=None, rel_tol: float = 1e-10,
+                  max_iter: int = 0, preconditioner="auto", ctx: Optional[Context] = None) -> Solution:
+    """solver.hpp:223-247 for meshes with Dirichlet faces, device-resident from the
+    assembly through the CG solve to the nodal scatter."""
+    ctx = ctx or Context.default()
+    r = assemble_system(mesh, f, g_dirichlet, g_neumann, coef, ctx)
+    u = np.empty(mesh.num_nodes(), dtype=np.float64)
+    it, rr = C.c_int64(), C.c_double()
+    o = _cg_options(rel_tol, max_iter, preconditioner)
+    _lib.check(_lib.lib().fl_solve_system(ctx.handle, r.handle, C.byref(o), u.ctypes.data, _lib.MEM_HOST,
+                                          C.byref(it), C.byref(rr)), "fl_solve_system")
+    return Solution(u, it.value, rr.value, r.partition())

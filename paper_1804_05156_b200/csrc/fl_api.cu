@@ -818,6 +818,122 @@ FL_API int fl_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_pt
     return FL_OK;
 }
 
+// ---- solve -----------------------------------------------------
+static int cg_check(const fl_cg_options* o) {
+    if (!o) return set_error(FL_ERR_ARGUMENT, "null options");
+    if (!(o->rel_tol > 0.0)) return set_error(FL_E_INVALID_PARAMETER, "rel_tol must be positive");
+    return FL_OK;
+}
+
+FL_API int fl_cg_solve(fl_ctx* ctx, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
+                       const double* values, const double* b, int mem, const fl_cg_options* opts,
+                       double* x, int64_t* iterations, double* relres, int32_t* converged) {
+    if (!ctx || !col_ptr || !x || !iterations || !relres || !converged || (n > 0 && !b))
+        return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (n < 0) return set_error(FL_E_SHAPE_MISMATCH, "cg_solve: negative size");
+    FL_TRY(cg_check(opts));
+    FL_CUDA(cudaSetDevice(ctx->device));
+    if (mem == FL_MEM_DEVICE)
+        return cg_solve_device(ctx, n, col_ptr, row_idx, values, b, opts->rel_tol, opts->max_iter,
+                               opts->preconditioner, x, iterations, relres, converged);
+    // host arrays: stage on the device
+    DevBuf dcp, dri, dva, db, dx;
+    auto release = [&]() {
+        dcp.release();
+        dri.release();
+        dva.release();
+        db.release();
+        dx.release();
+    };
+    int rc = copy_in(ctx, dcp, col_ptr, sizeof(int32_t) * ((size_t)n + 1), FL_MEM_HOST);
+    const int64_t nnz = n >= 0 ? col_ptr[n] : 0;
+    if (!rc) rc = copy_in(ctx, dri, row_idx, sizeof(int32_t) * (size_t)nnz, FL_MEM_HOST);
+    if (!rc) rc = copy_in(ctx, dva, values, sizeof(double) * (size_t)nnz, FL_MEM_HOST);
+    if (!rc) rc = copy_in(ctx, db, b, sizeof(double) * (size_t)n, FL_MEM_HOST);
+    if (!rc) rc = dx.ensure(sizeof(double) * (size_t)std::max(n, 1));
+    if (!rc)
+        rc = cg_solve_device(ctx, n, dcp.as<int32_t>(), dri.as<int32_t>(), dva.as<double>(),
+                             db.as<double>(), opts->rel_tol, opts->max_iter, opts->preconditioner,
+                             dx.as<double>(), iterations, relres, converged);
+    if (!rc && n > 0) {
+        cudaError_t e = cudaMemcpyAsync(x, dx.p, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost,
+                                        ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    cudaStreamSynchronize(ctx->stream);
+    release();
+    return rc;
+}
+
+FL_API int fl_matvec(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
+                     const int32_t* row_idx, const double* values, const double* x, double* y,
+                     int mem) {
+    if (!ctx || !col_ptr || (m > 0 && !y) || (n > 0 && !x)) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (m < 0 || n < 0) return set_error(FL_E_SHAPE_MISMATCH, "matvec: negative size");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    if (mem == FL_MEM_DEVICE) return matvec_device(ctx, m, n, col_ptr, row_idx, values, x, y);
+    DevBuf dcp, dri, dva, dx, dy;
+    const int64_t nnz = col_ptr[n];
+    int rc = copy_in(ctx, dcp, col_ptr, sizeof(int32_t) * ((size_t)n + 1), FL_MEM_HOST);
+    if (!rc) rc = copy_in(ctx, dri, row_idx, sizeof(int32_t) * (size_t)nnz, FL_MEM_HOST);
+    if (!rc) rc = copy_in(ctx, dva, values, sizeof(double) * (size_t)nnz, FL_MEM_HOST);
+    if (!rc) rc = copy_in(ctx, dx, x, sizeof(double) * (size_t)n, FL_MEM_HOST);
+    if (!rc) rc = dy.ensure(sizeof(double) * (size_t)std::max(m, 1));
+    if (!rc) rc = matvec_device(ctx, m, n, dcp.as<int32_t>(), dri.as<int32_t>(), dva.as<double>(),
+                                dx.as<double>(), dy.as<double>());
+    if (!rc && m > 0) {
+        cudaError_t e = cudaMemcpy(y, dy.p, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    dcp.release();
+    dri.release();
+    dva.release();
+    dx.release();
+    dy.release();
+    return rc;
+}
+
+FL_API int fl_solve_system(fl_ctx* ctx, fl_result* res, const fl_cg_options* opts, double* u,
+                           int mem, int64_t* iterations, double* relres) {
+    if (!ctx || !res || !u || !iterations || !relres) return set_error(FL_ERR_ARGUMENT, "null argument");
+    FL_TRY(cg_check(opts));
+    if (!(res->what & FL_OUT_SYSTEM)) return set_error(FL_ERR_ARGUMENT, "result holds no FL_OUT_SYSTEM");
+    fl_sizes z;
+    FL_TRY(fl_result_sizes(res, &z));
+    if (z.n != res->m) return set_error(FL_ERR_UNSUPPORTED, "fl_solve_system needs the whole mesh");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    DevBuf dx, du;
+    int32_t conv = 1;
+    int rc = dx.ensure(sizeof(double) * (size_t)std::max(z.n_free, 1));
+    if (!rc)
+        rc = cg_solve_device(ctx, z.n_free, res->arr[FL_AFF_COL_PTR].as<int32_t>(),
+                             res->arr[FL_AFF_ROW_IDX].as<int32_t>(), res->arr[FL_AFF_VALUES].as<double>(),
+                             res->arr[FL_B_F].as<double>(), opts->rel_tol, opts->max_iter,
+                             opts->preconditioner, dx.as<double>(), iterations, relres, &conv);
+    double* target = u;
+    if (!rc && mem != FL_MEM_DEVICE) {
+        rc = du.ensure(sizeof(double) * (size_t)std::max(z.n, 1));
+        target = du.as<double>();
+    }
+    if (!rc && z.n > 0) {
+        cudaError_t e = cudaMemcpyAsync(target, res->arr[FL_U0].p, sizeof(double) * (size_t)z.n,
+                                        cudaMemcpyDeviceToDevice, ctx->stream);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+        if (!rc) rc = scatter_free(ctx, z.n_free, res->arr[FL_FREE_NODES].as<int32_t>(), dx.as<double>(), target);
+        if (!rc && mem != FL_MEM_DEVICE) {
+            e = cudaMemcpyAsync(u, target, sizeof(double) * (size_t)z.n, cudaMemcpyDeviceToHost, ctx->stream);
+            if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+        }
+    }
+    cudaStreamSynchronize(ctx->stream);
+    dx.release();
+    du.release();
+    if (!rc && !conv)
+        return set_error(FL_E_MAX_ITER_EXCEEDED, "cg did not reach rel_tol in max_iter iterations");
+    return rc;
+}
+
 FL_API int fl_phase_cycles(fl_ctx* ctx, uint64_t* out6) {
     if (!ctx || !out6) return set_error(FL_ERR_ARGUMENT, "null argument");
     for (int i = 0; i < 6; ++i) out6[i] = 0;

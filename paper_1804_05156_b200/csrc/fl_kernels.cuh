@@ -83,6 +83,12 @@ int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
 int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out);
 int launch_boundary_faces(fl_ctx* ctx, fl_mesh* mesh, int64_t* n_faces);
 int launch_boundary_scatter(fl_ctx* ctx, fl_mesh* mesh, const int8_t* values, int8_t fill);
+int cg_solve_device(fl_ctx* ctx, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
+                    const double* values, const double* b, double rel_tol, int64_t max_iter,
+                    int precond, double* x_out, int64_t* iterations, double* relres, int32_t* converged);
+int scatter_free(fl_ctx* ctx, int32_t nf, const int32_t* free_nodes, const double* x, double* u);
+int matvec_device(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
+                  const double* values, const double* x, double* y);
 size_t column_smem_bytes();
 int column_tile_width();
 
