@@ -12,6 +12,7 @@
 //                                                    partition, A, b, Neumann, Dirichlet lift,
 //                                                    A(free, free), b_f -- one fused pass)
 //   femlite_b200::submatrix(a, rows, cols)           sparse.hpp:159    submatrix
+//   femlite_b200::matvec / cg_solve / solve_poisson  sparse.hpp:129, solver.hpp:63, :223
 //
 // Include it after the femlite headers.  Errors are rethrown as
 // femlite::Error with the reference's ErrorCode (the ABI status is
@@ -30,6 +31,7 @@
 
 #include "femlite/error.hpp"
 #include "femlite/mesh.hpp"
+#include "femlite/solver.hpp"
 #include "femlite/sparse.hpp"
 #include "femlite/system.hpp"
 #include "femlite_b200.h"
@@ -255,6 +257,72 @@ inline PoissonSystem poisson_system(const femlite::Mesh& mesh, const femlite::Po
     s.a_ff = r.matrix_ff();
     s.b_f = r.array<double>(FL_B_F, z.n_free_cols);
     return s;
+}
+
+/// sparse.hpp:129-141, bitwise
+inline std::vector<double> matvec(const femlite::CscMatrix& a, std::span<const double> x,
+                                  Context& ctx = Context::default_context()) {
+    if (static_cast<femlite::index_t>(x.size()) != a.n)
+        throw femlite::Error(femlite::ErrorCode::shape_mismatch, "matvec: vector length mismatch");
+    std::vector<double> y(static_cast<std::size_t>(a.m));
+    check(fl_matvec(ctx.get(), a.m, a.n, a.col_ptr.data(), a.row_idx.data(), a.values.data(), x.data(),
+                    y.data(), FL_MEM_HOST),
+          "fl_matvec");
+    return y;
+}
+
+/// solver.hpp:63-136 on the GPU (dot products are tree reductions: iterates
+/// agree with the reference to rounding)
+inline femlite::CgResult cg_solve(const femlite::CscMatrix& a, std::span<const double> b,
+                                  const femlite::SolveOptions& opts = {},
+                                  Context& ctx = Context::default_context()) {
+    if (a.m != a.n) throw femlite::Error(femlite::ErrorCode::shape_mismatch, "cg_solve: matrix not square");
+    if (static_cast<femlite::index_t>(b.size()) != a.n)
+        throw femlite::Error(femlite::ErrorCode::shape_mismatch, "cg_solve: vector length mismatch");
+    fl_cg_options o{opts.rel_tol, opts.max_iter,
+                    opts.preconditioner == femlite::Preconditioner::none     ? 0
+                    : opts.preconditioner == femlite::Preconditioner::jacobi ? 1
+                                                                            : 2,
+                    0};
+    femlite::CgResult r;
+    r.x.resize(b.size());
+    int64_t it = 0;
+    int32_t conv = 1;
+    check(fl_cg_solve(ctx.get(), a.n, a.col_ptr.data(), a.row_idx.data(), a.values.data(), b.data(),
+                      FL_MEM_HOST, &o, r.x.data(), &it, &r.relres, &conv),
+          "fl_cg_solve");
+    r.iterations = static_cast<femlite::index_t>(it);
+    r.converged = conv != 0;
+    return r;
+}
+
+/// solver.hpp:223-247 for meshes with Dirichlet faces: assembly, CG and the
+/// nodal scatter device-resident; throws max_iter_exceeded like solve_reduced
+inline femlite::Solution solve_poisson(const femlite::Mesh& mesh, const femlite::PoissonProblem& pb,
+                                       const femlite::SolveOptions& opts = {},
+                                       Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    std::vector<double> fs, gd, gn;
+    fl_field ff = detail::none(), fd = detail::none(), fn = detail::none();
+    const fl_field n = detail::none();
+    if (pb.f) ff = detail::samples(fs = detail::sample(mesh, pb.f, 0));
+    if (pb.g_dirichlet) fd = detail::samples(gd = detail::sample_nodes(mesh, pb.g_dirichlet));
+    if (pb.g_neumann) fn = detail::samples(gn = detail::sample(mesh, pb.g_neumann, 3));
+    check(fl_assemble(ctx.get(), m.m, &ff, &n, &fd, &fn, FL_OUT_SYSTEM, r.r), "fl_assemble");
+    fl_cg_options o{opts.rel_tol, opts.max_iter,
+                    opts.preconditioner == femlite::Preconditioner::none     ? 0
+                    : opts.preconditioner == femlite::Preconditioner::jacobi ? 1
+                                                                            : 2,
+                    0};
+    femlite::Solution sol;
+    sol.u.resize(static_cast<std::size_t>(mesh.num_nodes()));
+    int64_t it = 0;
+    check(fl_solve_system(ctx.get(), r.r, &o, sol.u.data(), FL_MEM_HOST, &it, &sol.final_relres),
+          "fl_solve_system");
+    sol.iterations = static_cast<femlite::index_t>(it);
+    sol.partition = detail::partition_of(mesh, r);
+    return sol;
 }
 
 /// sparse.hpp:159 (strictly increasing index sets, validated on the GPU)

@@ -6,12 +6,14 @@
 // Exit 0 = every comparison bitwise equal (CscMatrix::operator==, memcmp).
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <numbers>
 #include <vector>
 
 #include "femlite/assembly.hpp"
 #include "femlite/mesh.hpp"
+#include "femlite/solver.hpp"
 #include "femlite/sparse.hpp"
 #include "femlite/system.hpp"
 #include "femlite_b200_adapter.hpp"
@@ -89,6 +91,18 @@ void run(const char* name, const femlite::Mesh& mesh) {
         expect(same(s.dirichlet.b, ds.b), "poisson_system b - A u0", name);
         expect(s.a_ff == aff, "poisson_system A(free, free)", name);
         expect(same(s.b_f, bf), "poisson_system b_f", name);
+        // the solve after the path (tolerance: CG dot products differ in order)
+        expect(same(matvec(a, bn), femlite_b200::matvec(a, bn)), "matvec", name);
+        SolveOptions so;
+        const Solution ref_sol = femlite::solve_poisson(mesh, pb, so);
+        const Solution gpu_sol = femlite_b200::solve_poisson(mesh, pb, so);
+        double worst = 0.0, scale = 1.0;
+        for (std::size_t k = 0; k < ref_sol.u.size(); ++k) {
+            worst = std::max(worst, std::abs(ref_sol.u[k] - gpu_sol.u[k]));
+            scale = std::max(scale, std::abs(ref_sol.u[k]));
+        }
+        expect(worst <= 1e-7 * scale, "solve_poisson u (1e-7 relative)", name);
+        expect(std::abs(ref_sol.iterations - gpu_sol.iterations) <= 2, "solve_poisson iterations", name);
         // general submatrix
         std::vector<index_t> rows, cols;
         for (index_t k = 0; k < a.m; k += 2) rows.push_back(k);
