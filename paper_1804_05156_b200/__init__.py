@@ -17,7 +17,8 @@ the C-ABI of include/femlite_b200.h); importing does not touch the GPU.
 """
 from .api import (AssemblyResult, AssemblyStrategy, BoundaryPartition, CgResult, CscMatrix,
                   DirichletSystem, PoissonSystem, Solution, assemble, assemble_blockwise,
-                  assemble_load, assemble_system, apply_neumann, cg_solve, matvec, partition_boundary,
+                  assemble_load, assemble_system, apply_neumann, cg_solve, from_triplets, matvec,
+                  partition_boundary,
                   poisson_system, run, solve_poisson, submatrix)
 from .context import Context
 from .errors import Error, ErrorCode
@@ -32,5 +33,5 @@ __all__ = [
     "boundary_face_mask", "classifier_dirichlet", "classifier_lshape", "classifier_mixed",
     "classifier_neumann", "flag_generated", "generate_mesh", "make_mesh", "partition_boundary",
     "poisson_system", "run", "set_boundary_flags", "submatrix", "cg_solve", "matvec", "solve_poisson",
-    "Solution",
+    "Solution", "from_triplets",
 ]

@@ -413,3 +413,24 @@ def solve_poisson(mesh: Mesh, f, g_dirichlet, g_neumann=None, coef=None, rel_tol
     _lib.check(_lib.lib().fl_solve_system(ctx.handle, r.handle, C.byref(o), u.ctypes.data, _lib.MEM_HOST,
                                           C.byref(it), C.byref(rr)), "fl_solve_system")
     return Solution(u, it.value, rr.value, r.partition())
+
+
+def from_triplets(m: int, n: int, ii, jj, ss, ctx: Optional[Context] = None) -> CscMatrix:
+    """sparse.hpp:61: COO with duplicates -> CSC on the
+    GPU; duplicates summed in their original order, exact zeros dropped."""
+    ctx = ctx or Context.default()
+    ii = np.ascontiguousarray(ii, dtype=np.int32)
+    jj = np.ascontiguousarray(jj, dtype=np.int32)
+    ss = np.ascontiguousarray(ss, dtype=np.float64)
+    if not (ii.shape == jj.shape == ss.shape):
+        raise Error(ErrorCode.shape_mismatch, "triplet arrays differ in length")
+    res = AssemblyResult(ctx)
+    _lib.check(_lib.lib().fl_from_triplets(ctx.handle, int(m), int(n), ii.size,
+                                           ii.ctypes.data if ii.size else None,
+                                           jj.ctypes.data if jj.size else None,
+                                           ss.ctypes.data if ss.size else None, _lib.MEM_HOST,
+                                           res.handle), "fl_from_triplets")
+    s = res.sizes()
+    return CscMatrix(int(m), int(n), res.array(_lib.A_COL_PTR, np.int32, n + 1),
+                     res.array(_lib.A_ROW_IDX, np.int32, s.nnz),
+                     res.array(_lib.A_VALUES, np.float64, s.nnz))

@@ -866,6 +866,28 @@ FL_API int fl_cg_solve(fl_ctx* ctx, int32_t n, const int32_t* col_ptr, const int
     return rc;
 }
 
+FL_API int fl_from_triplets(fl_ctx* ctx, int32_t m, int32_t n, int64_t count, const int32_t* ii,
+                            const int32_t* jj, const double* ss, int mem, fl_result* res) {
+    if (!ctx || !res || (count > 0 && (!ii || !jj || !ss))) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (m < 0 || n < 0) return set_error(FL_E_SHAPE_MISMATCH, "negative matrix dimension");
+    if (count < 0 || count >= ((int64_t)1 << 31))
+        return set_error(FL_ERR_UNSUPPORTED, "triplet count outside [0, 2^31)");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    fl_result_ext* x = ext_of(res);
+    x->last_valid = false;
+    const int32_t *di = ii, *dj = jj;
+    const double* ds = ss;
+    if (mem != FL_MEM_DEVICE) {
+        FL_TRY(copy_in(ctx, x->stage.sub[0], ii, sizeof(int32_t) * (size_t)count, FL_MEM_HOST));
+        FL_TRY(copy_in(ctx, x->stage.sub[1], jj, sizeof(int32_t) * (size_t)count, FL_MEM_HOST));
+        FL_TRY(copy_in(ctx, x->stage.sub[2], ss, sizeof(double) * (size_t)count, FL_MEM_HOST));
+        di = x->stage.sub[0].as<int32_t>();
+        dj = x->stage.sub[1].as<int32_t>();
+        ds = x->stage.sub[2].as<double>();
+    }
+    return launch_from_triplets(ctx, m, n, count, di, dj, ds, res);
+}
+
 FL_API int fl_matvec(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
                      const int32_t* row_idx, const double* values, const double* x, double* y,
                      int mem) {
