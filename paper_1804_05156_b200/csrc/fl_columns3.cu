@@ -378,17 +378,18 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                             // bit b of the concatenated pass masks = item itm[b / L][b % L]:
                             // ascending bits walk (i, lane) in the reference's order
                             const uint4 mk4 = sm.msk[h];
-                            const double* flat = &sm.itm[0][0];
-                            uint64_t w0, w1 = 0;
-                            if constexpr (L == 32) {
-                                w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << 32);
-                                w1 = (uint64_t)mk4.z | ((uint64_t)mk4.w << 32);
-                            } else {
-                                w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) | ((uint64_t)mk4.z << (2 * L));
+                            if constexpr (L == 32) {  // pass by pass, lanes ascending
+                                const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+#pragma unroll
+                                for (int i = 0; i < NV; ++i)
+                                    for (unsigned mm = mk[i]; mm; mm &= mm - 1)
+                                        acc = acc + sm.itm[i][__ffs(mm) - 1];
+                            } else {  // the passes' L-bit masks concatenated: bit b = itm[b / L][b % L]
+                                const double* flat = &sm.itm[0][0];
+                                const uint64_t w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) |
+                                                    ((uint64_t)mk4.z << (2 * L));
+                                for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
                             }
-                            for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
-                            if constexpr (L == 32)
-                                for (uint64_t w = w1; w; w &= w - 1) acc = acc + flat[63 + __ffsll(w)];
                         }
                         int rk = 0;  // rows below r; unused entries (-1) compare as huge
                         const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
