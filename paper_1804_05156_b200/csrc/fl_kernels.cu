@@ -360,9 +360,10 @@ __device__ __forceinline__ uint32_t slot_hash(int32_t row) {
     return ((uint32_t)row * 2654435761u) >> 24;  // 8 bits
 }
 
+// -1: the column has more distinct rows than the table holds (DERR_OVERFLOW)
 __device__ __forceinline__ int find_or_insert(WarpSmem& ws, int32_t row) {
     uint32_t h = slot_hash(row);
-    while (true) {
+    for (int probe = 0; probe < kMaxSlots; ++probe) {
         const int32_t prev = atomicCAS(&ws.keys[h], kEmpty, row);
         if (prev == kEmpty) {
             ws.acc[h] = -0.0;   // -0.0 + x == x for every x: the fold starts at
@@ -372,12 +373,16 @@ __device__ __forceinline__ int find_or_insert(WarpSmem& ws, int32_t row) {
         if (prev == row) return (int)h;
         h = (h + 1) & (kHS - 1);
     }
+    return -1;
 }
 
 __device__ __forceinline__ int find_slot(const WarpSmem& ws, int32_t row) {
     uint32_t h = slot_hash(row);
-    while (ws.keys[h] != row) h = (h + 1) & (kHS - 1);
-    return (int)h;
+    for (int probe = 0; probe < kHS; ++probe) {
+        if (ws.keys[h] == row) return (int)h;
+        h = (h + 1) & (kHS - 1);
+    }
+    return -1;
 }
 
 __device__ __forceinline__ double field_at_node(const FieldDesc& g, const double* nodes, int dim,
@@ -484,11 +489,6 @@ __device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lan
     if (lane == 0) ws.n_a = ws.n_ff = 0;
     __syncwarp();
 
-    if ((int64_t)m * D + 1 > kMaxSlots && p.want_a) {
-        if (lane == 0) atomicOr(p.err, DERR_OVERFLOW);
-        b_out = bmod_out = u0_out = 0.0;
-        return;
-    }
 
     Lane<D> L;
     ElemCol<D> ec;
@@ -511,9 +511,13 @@ __device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lan
             __syncwarp();
             if (L.valid && lane == __ffs(g) - 1) {
                 const int slot = find_or_insert(ws, key);
-                double a = ws.acc[slot];
-                for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
-                ws.acc[slot] = a;
+                if (slot >= 0) {
+                    double a = ws.acc[slot];
+                    for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
+                    ws.acc[slot] = a;
+                } else {
+                    atomicOr(p.err, DERR_OVERFLOW);
+                }
             }
             __syncwarp();
         }
@@ -582,9 +586,11 @@ __device__ void column_warp(const ColParams& p, int32_t c, WarpSmem& ws, int lan
                     __syncwarp();
                     if (act && lane == __ffs(g) - 1) {
                         const int slot = find_slot(ws, key);
-                        double a = ws.tacc[slot];
-                        for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
-                        ws.tacc[slot] = a;
+                        if (slot >= 0) {
+                            double a = ws.tacc[slot];
+                            for (unsigned mm = g; mm; mm &= mm - 1) a = a + ws.stage[__ffs(mm) - 1];
+                            ws.tacc[slot] = a;
+                        }
                     }
                     __syncwarp();
                 }
