@@ -428,6 +428,7 @@ FL_API int fl_result_destroy(fl_result* r) {
     r->tile_off.release();
     r->colcnt.release();
     for (auto& b : r->erec) b.release();
+    for (auto& b : r->hyb) b.release();
     r->counters.release();
     fl_result_ext* x = ext_of(r);
     x->stage.f.release();
@@ -501,7 +502,11 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     const char kk = kern ? kern[0] : '0';
     const int64_t fast_rows = mesh->dim == 2 ? 12 : 24;
     const int64_t bound = std::max<int64_t>(mesh->nnz_bound, 1);
-    const size_t cap = (size_t)(kk == '1' ? bound : std::min<int64_t>(bound, fast_rows * std::max(NC, 1)));
+    // columns above the register kernel's valence go to the hybrid pass, sized
+    // by the plan's bound
+    const bool hyb = mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc);
+    const size_t cap = (size_t)(kk == '1' || hyb ? bound
+                                                 : std::min<int64_t>(bound, fast_rows * std::max(NC, 1)));
     uint32_t* counters = res->counters.as<uint32_t>();
     FL_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * CNT_WORDS, s));
     if (want_a) {
@@ -599,6 +604,8 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
             } else if (k == '2' || p.need_lift || (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)) {
                 FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
+            } else if (mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc)) {
+                FL_TRY(launch_hybrid(ctx, mesh->dim, p, mesh, res, k != '3'));
             } else {
                 FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res, k != '3'));
             }

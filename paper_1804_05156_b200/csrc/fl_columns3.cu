@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 col_range(q + C::GPW, p0n, mn);
                 key_next = (g < mn && mn <= L) ? __ldg(p.inc + p0n + g) : 0xFFFFFFFFu;
             }
-            if (m > L) {
-                bad = true;
+            if (m > L) {  // hybrid: the general kernel takes the column afterwards
+                if (!p.hybrid) bad = true;
                 m = 0;
                 key = 0xFFFFFFFFu;
             }
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
 }
 
 template <int D, int L, bool PRE>
-static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
+static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
     using C = V3<D, L>;
     FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
     if (ctx->profile) {
@@ -530,17 +530,20 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res) {
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
-    return finish_staging(ctx, p, C::WTC);
+    return finish ? finish_staging(ctx, p, C::WTC) : FL_OK;
 }
 
 // kmax: the plan's largest node valence; need_lift meshes use the tiled kernel.
 // pre: element-first records (default) or per-incidence geometry in the kernel.
-int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre) {
+int columns3_lanes(int dim, int kmax) { return dim == 2 ? (kmax <= 8 ? 8 : 16) : 32; }
+
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre, bool finish) {
     if (dim == 2) {
-        if (kmax <= 8) return pre ? launch3<2, 8, true>(ctx, p, res) : launch3<2, 8, false>(ctx, p, res);
-        return pre ? launch3<2, 16, true>(ctx, p, res) : launch3<2, 16, false>(ctx, p, res);
+        if (kmax <= 8)
+            return pre ? launch3<2, 8, true>(ctx, p, res, finish) : launch3<2, 8, false>(ctx, p, res, finish);
+        return pre ? launch3<2, 16, true>(ctx, p, res, finish) : launch3<2, 16, false>(ctx, p, res, finish);
     }
-    return pre ? launch3<3, 32, true>(ctx, p, res) : launch3<3, 32, false>(ctx, p, res);
+    return pre ? launch3<3, 32, true>(ctx, p, res, finish) : launch3<3, 32, false>(ctx, p, res, finish);
 }
 
 }  // namespace fl

@@ -182,9 +182,10 @@ k_inc_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage,
 // Sort each node's incidence keys ascending = (j, t) order.  Segments are
 // short (2-D ~6, 3-D Kuhn 24): insertion sort per thread.
 __global__ void k_inc_sort(int32_t n_nodes, const int32_t* __restrict__ inc_ptr,
-                           uint32_t* __restrict__ inc) {
-    const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= n_nodes) return;
+                           uint32_t* __restrict__ inc, const int32_t* __restrict__ list) {
+    const int32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_nodes) return;
+    const int32_t c = list ? list[q] : q;
     const int32_t p0 = inc_ptr[c], p1 = inc_ptr[c + 1];
     for (int32_t a = p0 + 1; a < p1; ++a) {
         const uint32_t key = inc[a];
@@ -728,9 +729,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
         __syncthreads();
         const int64_t tile = s_tile;
         if (tile >= p.n_tiles) break;
-        const int64_t lc64 = tile * kWarps + w;
-        const bool has = lc64 < p.n_cols;
-        const int32_t lc = (int32_t)lc64, c = p.c_begin + lc;
+        const int64_t q64 = tile * kWarps + w;
+        const bool has = p.col_list ? q64 < p.n_list : q64 < p.n_cols;
+        const int32_t lc = p.col_list ? (has ? p.col_list[q64] : 0) : (int32_t)q64;
+        const int32_t c = p.c_begin + lc;
         double b = 0.0, bmod = 0.0, u0 = 0.0;
         if (has) {
             column_warp<D>(p, c, ws, lane, b, bmod, u0);
@@ -769,14 +771,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
                         p.row_idx[off_a + q] = ws.out_rows[q];
                         p.values[off_a + q] = ws.out_vals[q];
                     }
-                    if (lane == 0) p.col_ptr[lc + 1] = (int32_t)(off_a + na);
+                    if (lane == 0 && p.col_list) {  // hybrid: counts / offsets per listed column
+                        p.ov_cnt[q64] = na;
+                        p.ov_cnt[p.n_list + q64] = nf;
+                        p.ov_off[q64] = (int32_t)off_a;
+                        p.ov_off[p.n_list + q64] = (int32_t)off_f;
+                    } else if (lane == 0) {
+                        p.col_ptr[lc + 1] = (int32_t)(off_a + na);
+                    }
                     if (p.want_sys) {
                         const int32_t fc = p.fidx[c] - free_base(p);
                         for (int q = lane; q < nf; q += 32) {
                             p.ff_row_idx[off_f + q] = ws.ff_rows[q];
                             p.ff_values[off_f + q] = ws.ff_vals[q];
                         }
-                        if (lane == 0 && fc >= 0) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + nf);
+                        if (lane == 0 && fc >= 0 && !p.col_list) p.ff_col_ptr[fc + 1] = (int32_t)(off_f + nf);
                     }
                 }
             }
@@ -960,7 +969,7 @@ int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh) {
     const int32_t nc = mesh->col_end - mesh->col_begin;
     if (nc > 0) {
         k_inc_sort<<<div_up(nc, 128), 128, 0, ctx->stream>>>(nc, mesh->inc_ptr.as<int32_t>(),
-                                                            mesh->inc.as<uint32_t>());
+                                                            mesh->inc.as<uint32_t>(), nullptr);
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
@@ -986,6 +995,177 @@ int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out) {
         res->n, res->col_begin, res->m, want_a, want_sys, res->arr[FL_A_COL_PTR].as<int32_t>(),
         want_sys ? res->fidx.as<int32_t>() + (size_t)res->m + 1 : nullptr,
         res->arr[FL_AFF_COL_PTR].as<int32_t>(), dev_out);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hybrid column pass: register kernel for columns of <= L incidences, the
+// general kernel for the rest (unstructured meshes), per-column placement
+// ---------------------------------------------------------------------------
+__global__ void k_list_big(int32_t n_cols, int32_t n_nodes, int dim, int lanes,
+                           const int32_t* __restrict__ inc_ptr, int32_t* __restrict__ list,
+                           int32_t* __restrict__ ovidx, unsigned long long* __restrict__ acc) {
+    for (int32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < n_cols; lc += gridDim.x * blockDim.x) {
+        const int32_t m = inc_ptr[lc + 1] - inc_ptr[lc];
+        int32_t q = -1;
+        if (m > lanes) {
+            q = (int32_t)atomicAdd(acc, 1ull);
+            list[q] = lc;
+            const int64_t b = (int64_t)m * dim + 1;
+            atomicAdd(acc + 1, (unsigned long long)(b < n_nodes ? b : n_nodes));
+        }
+        ovidx[lc] = q;
+    }
+}
+
+// entries of each owned column: register-kernel tiles (in-tile inclusive
+// counts) or the general kernel's listed columns
+__global__ void k_hyb_counts(ColParams p, int tc, const int32_t* __restrict__ ovidx, int32_t* __restrict__ ca,
+                             int32_t* __restrict__ cf) {
+    for (int32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < p.n_cols; lc += gridDim.x * blockDim.x) {
+        const int32_t q = ovidx[lc];
+        int32_t a, f = 0;
+        if (q >= 0) {
+            a = p.ov_cnt[q];
+            f = p.want_sys ? p.ov_cnt[p.n_list + q] : 0;
+        } else {
+            const bool first = lc % tc == 0;
+            a = p.colcnt_a[lc] - (first ? 0 : p.colcnt_a[lc - 1]);
+            if (p.want_sys) f = p.colcnt_f[lc] - (first ? 0 : p.colcnt_f[lc - 1]);
+        }
+        ca[lc] = a;
+        cf[lc] = f;
+    }
+}
+
+// warp per column: copy its entries from the tile staging or the overflow
+// staging to col_ptr / the A(free,free) position
+__global__ void k_hyb_copy(ColParams p, int tc, const int32_t* __restrict__ ovidx,
+                           const int32_t* __restrict__ pf, const int32_t* __restrict__ ov_row,
+                           const double* __restrict__ ov_val, const int32_t* __restrict__ ovf_row,
+                           const double* __restrict__ ovf_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int32_t fb = free_base(p);
+    for (int64_t lc64 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; lc64 < p.n_cols; lc64 += nw) {
+        const int32_t lc = (int32_t)lc64;
+        const int32_t q = ovidx[lc];
+        const int32_t da = p.col_ptr[lc], na = p.col_ptr[lc + 1] - da;
+        const int32_t df = pf[lc], nf = pf[lc + 1] - df;
+        if ((int64_t)da + na > p.cap_a || (int64_t)df + nf > p.cap_ff) {
+            if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
+            continue;
+        }
+        const int32_t* ra;
+        const double* va;
+        const int32_t* rf;
+        const double* vf;
+        if (q >= 0) {
+            ra = ov_row + p.ov_off[q];
+            va = ov_val + p.ov_off[q];
+            rf = ovf_row + p.ov_off[p.n_list + q];
+            vf = ovf_val + p.ov_off[p.n_list + q];
+        } else {
+            const int64_t t = lc / tc;
+            const bool first = lc % tc == 0;
+            const int64_t sa = t * p.tile_cap + (first ? 0 : p.colcnt_a[lc - 1]);
+            ra = p.st_a_row + sa;
+            va = p.st_a_val + sa;
+            const int64_t sf = t * p.tile_cap + (first || !p.want_sys ? 0 : p.colcnt_f[lc - 1]);
+            rf = p.st_f_row + sf;
+            vf = p.st_f_val + sf;
+        }
+        for (int k = lane; k < na; k += 32) {
+            p.row_idx[da + k] = ra[k];
+            p.values[da + k] = va[k];
+        }
+        if (p.want_sys) {
+            for (int k = lane; k < nf; k += 32) {
+                p.ff_row_idx[df + k] = rf[k];
+                p.ff_values[df + k] = vf[k];
+            }
+            const int32_t fc = p.fidx[p.c_begin + lc];
+            if (lane == 0 && fc >= 0) p.ff_col_ptr[fc - fb + 1] = df + nf;
+        }
+    }
+}
+
+int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* res, bool pre) {
+    const cudaStream_t s = ctx->stream;
+    const int lanes = columns3_lanes(dim, mesh->max_inc);
+    const int32_t NC = p.n_cols;
+    // 1. the columns above the register kernel's valence, and their output bound
+    FL_TRY(res->hyb[0].ensure(sizeof(int32_t) * 2 * ((size_t)NC + 1)));  // list | ovidx
+    FL_TRY(res->hyb[1].ensure(sizeof(unsigned long long) * 2));
+    int32_t* list = res->hyb[0].as<int32_t>();
+    int32_t* ovidx = list + NC + 1;
+    unsigned long long* acc = res->hyb[1].as<unsigned long long>();
+    FL_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 2, s));
+    k_list_big<<<std::max(1, std::min(div_up(NC, 256), ctx->sm_count * 8)), 256, 0, s>>>(
+        NC, p.n_nodes, dim, lanes, p.inc_ptr, list, ovidx, acc);
+    count_launch(ctx);
+    unsigned long long* h = static_cast<unsigned long long*>(ctx->pinned);
+    FL_CUDA(cudaMemcpyAsync(h, acc, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    const int32_t n_list = (int32_t)h[0];
+    const int64_t bound = std::max<int64_t>((int64_t)h[1], 1);
+    // 2. the register kernel over every column (listed ones left empty)
+    p.hybrid = true;
+    FL_TRY(launch_columns3(ctx, dim, p, mesh->max_inc, res, pre, false));
+    // 3. the general kernel over the listed columns into overflow staging
+    ColParams q = p;
+    q.hybrid = false;
+    q.col_list = list;
+    q.n_list = n_list;
+    FL_TRY(res->hyb[2].ensure(sizeof(int32_t) * 4 * ((size_t)n_list + 1)));
+    q.ov_cnt = res->hyb[2].as<int32_t>();
+    q.ov_off = q.ov_cnt + 2 * ((size_t)n_list + 1);
+    for (int k = 0; k < 4; ++k)
+        FL_TRY(res->hyb[3 + k].ensure((k % 2 ? sizeof(double) : sizeof(int32_t)) * (size_t)bound));
+    q.row_idx = res->hyb[3].as<int32_t>();
+    q.values = res->hyb[4].as<double>();
+    q.ff_row_idx = res->hyb[5].as<int32_t>();
+    q.ff_values = res->hyb[6].as<double>();
+    q.cap_a = q.want_a ? bound : 0;
+    q.cap_ff = q.want_sys ? bound : 0;
+    if (n_list > 0) {
+        k_inc_sort<<<div_up(n_list, 128), 128, 0, s>>>(n_list, p.inc_ptr, const_cast<uint32_t*>(p.inc), list);
+        count_launch(ctx);
+        const int tw = column_tile_width();
+        q.n_tiles = (n_list + tw - 1) / tw;
+        FL_TRY(res->tile_status.ensure(sizeof(uint64_t) * ((size_t)q.n_tiles + 1)));
+        FL_CUDA(cudaMemsetAsync(res->tile_status.p, 0, sizeof(uint64_t) * ((size_t)q.n_tiles + 1), s));
+        q.tile_status = res->tile_status.as<uint64_t>();
+        FL_CUDA(cudaMemsetAsync(q.ticket, 0, sizeof(uint32_t), s));
+        FL_TRY(launch_columns(ctx, dim, q));
+    }
+    // 4. per-column placement
+    if (!p.want_a) return FL_OK;
+    const int tc = dim == 2 ? 32 : 8;  // the register kernel's columns per tile (V3::WTC)
+    FL_TRY(res->hyb[7].ensure(sizeof(int32_t) * 3 * ((size_t)NC + 1)));
+    int32_t* ca = res->hyb[7].as<int32_t>();
+    int32_t* cf = ca + NC + 1;
+    int32_t* pf = cf + NC + 1;
+    ColParams r = p;
+    r.ov_cnt = q.ov_cnt;
+    r.ov_off = q.ov_off;
+    r.n_list = n_list;
+    const int g = std::max(1, std::min(div_up(NC, 256), ctx->sm_count * 8));
+    k_hyb_counts<<<g, 256, 0, s>>>(r, tc, ovidx, ca, cf);
+    count_launch(ctx);
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(NC)));
+    const int32_t* cac = ca;
+    FL_CUDA(launch_scan<int32_t>(NC, [cac] __device__(int64_t i) { return (int64_t)cac[i]; }, p.col_ptr,
+                                 ctx->scan_ws.p, s));
+    const int32_t* cfc = cf;
+    FL_CUDA(launch_scan<int32_t>(NC, [cfc] __device__(int64_t i) { return (int64_t)cfc[i]; }, pf,
+                                 ctx->scan_ws.p, s));
+    count_launch(ctx, 2);
+    const int64_t warps = std::min<int64_t>(NC, (int64_t)ctx->sm_count * 64);
+    k_hyb_copy<<<(int)std::max<int64_t>(1, (warps * 32 + 255) / 256), 256, 0, s>>>(
+        r, tc, ovidx, pf, q.row_idx, q.values, q.ff_row_idx, q.ff_values);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;

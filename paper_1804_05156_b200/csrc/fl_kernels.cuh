@@ -59,6 +59,15 @@ struct ColParams {
     double* srec;
     double* lrec;
     const uint8_t* emark;  // sharded: records only for elements touching owned columns
+    // hybrid pass (columns above the fast kernels' valence): the register kernel
+    // leaves them empty (hybrid); the general kernel then runs on col_list only,
+    // writing its entries to overflow staging and per-listed-column counts /
+    // offsets into ov_cnt / ov_off ([2][n_list]: A, A(free,free))
+    bool hybrid;
+    const int32_t* col_list;
+    int32_t n_list;
+    int32_t* ov_cnt;
+    int32_t* ov_off;
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
@@ -76,7 +85,10 @@ int launch_submatrix(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
 int launch_selftest_div(fl_ctx* ctx, int64_t n, const double* a, const double* b, double* qf,
                         double* qi);
 int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res);
-int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre);
+int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre,
+                    bool finish = true);
+int columns3_lanes(int dim, int kmax);
+int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* res, bool pre);
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
 int finish_staging(fl_ctx* ctx, ColParams& p, int tc);
 int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh);
