@@ -45,6 +45,7 @@ SIGNATURES = {
     "fl_cg_solve": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "fl_solve_system": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "fl_from_triplets": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp, C.c_int, _vp]),
+    "fl_solve_neumann": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp, _vp, C.c_int, _vp, _vp]),
     "fl_matvec": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_int]),
     "fl_boundary_faces_copy": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),
     "fl_mesh_set_boundary_flags": (C.c_int, [_vp, _vp, _vp, C.c_int8, C.c_int]),

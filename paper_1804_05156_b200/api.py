@@ -402,16 +402,30 @@ def cg_solve(a: CscMatrix, b, rel_tol: float = 1e-10, max_iter: int = 0, precond
 
 
 def solve_poisson(mesh: Mesh, f, g_dirichlet, g_neumann=None, coef=None, rel_tol: float = 1e-10,
-                  max_iter: int = 0, preconditioner="auto", ctx: Optional[Context] = None) -> Solution:
-    """solver.hpp:223-247 for meshes with Dirichlet faces, device-resident from the
-    assembly through the CG solve to the nodal scatter."""
+                  max_iter: int = 0, preconditioner="auto", pin_node: int = 0,
+                  ctx: Optional[Context] = None) -> Solution:
+    """solver.hpp:223-276, device-resident from the assembly through the CG solve
+    to the nodal vector: with Dirichlet faces the free-node system (lift, A_ff,
+    b_f); without them the pure-Neumann path (compatibility, pinned node,
+    zero-average shift)."""
     ctx = ctx or Context.default()
-    r = assemble_system(mesh, f, g_dirichlet, g_neumann, coef, ctx)
+    o = _cg_options(rel_tol, max_iter, preconditioner)
     u = np.empty(mesh.num_nodes(), dtype=np.float64)
     it, rr = C.c_int64(), C.c_double()
-    o = _cg_options(rel_tol, max_iter, preconditioner)
-    _lib.check(_lib.lib().fl_solve_system(ctx.handle, r.handle, C.byref(o), u.ctypes.data, _lib.MEM_HOST,
-                                          C.byref(it), C.byref(rr)), "fl_solve_system")
+    probe = run(mesh, _lib.OUT_PARTITION, ctx=ctx)
+    if probe.sizes().n_dir_faces > 0:
+        if g_dirichlet is None:
+            raise Error(ErrorCode.invalid_parameter,
+                        "mesh has Dirichlet faces but the problem provides no g_dirichlet")
+        r = assemble_system(mesh, f, g_dirichlet, g_neumann, coef, ctx)
+        _lib.check(_lib.lib().fl_solve_system(ctx.handle, r.handle, C.byref(o), u.ctypes.data,
+                                              _lib.MEM_HOST, C.byref(it), C.byref(rr)), "fl_solve_system")
+    else:
+        r = run(mesh, _lib.OUT_STIFFNESS | _lib.OUT_LOAD | _lib.OUT_PARTITION, f=f, coef=coef,
+                g_neumann=g_neumann, ctx=ctx)
+        _lib.check(_lib.lib().fl_solve_neumann(ctx.handle, mesh.device(ctx).handle, r.handle, int(pin_node),
+                                               C.byref(o), u.ctypes.data, _lib.MEM_HOST, C.byref(it),
+                                               C.byref(rr)), "fl_solve_neumann")
     return Solution(u, it.value, rr.value, r.partition())
 
 

@@ -895,6 +895,43 @@ FL_API int fl_from_triplets(fl_ctx* ctx, int32_t m, int32_t n, int64_t count, co
     return launch_from_triplets(ctx, m, n, count, di, dj, ds, res);
 }
 
+FL_API int fl_solve_neumann(fl_ctx* ctx, fl_mesh* mesh, fl_result* res, int32_t pin,
+                            const fl_cg_options* opts, double* u, int mem, int64_t* iterations,
+                            double* relres) {
+    if (!ctx || !mesh || !res || !u || !iterations || !relres)
+        return set_error(FL_ERR_ARGUMENT, "null argument");
+    FL_TRY(cg_check(opts));
+    if ((res->what & (FL_OUT_STIFFNESS | FL_OUT_LOAD)) != (FL_OUT_STIFFNESS | FL_OUT_LOAD))
+        return set_error(FL_ERR_ARGUMENT, "result needs FL_OUT_STIFFNESS | FL_OUT_LOAD");
+    fl_sizes z;
+    FL_TRY(fl_result_sizes(res, &z));
+    if (z.n != res->m || res->m != mesh->n_nodes)
+        return set_error(FL_ERR_UNSUPPORTED, "fl_solve_neumann needs the whole mesh");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    DevBuf du;
+    double* target = u;
+    int rc = FL_OK;
+    if (mem != FL_MEM_DEVICE) {
+        rc = du.ensure(sizeof(double) * (size_t)std::max(z.n, 1));
+        target = du.as<double>();
+    }
+    int32_t conv = 1;
+    if (!rc)
+        rc = solve_neumann_device(ctx, mesh->dim, z.n, mesh->n_elems, mesh->nodes.as<double>(),
+                                  mesh->elems.as<int32_t>(), res->arr[FL_A_COL_PTR].as<int32_t>(),
+                                  res->arr[FL_A_ROW_IDX].as<int32_t>(), res->arr[FL_A_VALUES].as<double>(),
+                                  res->arr[FL_B].as<double>(), pin, opts->rel_tol, opts->max_iter,
+                                  opts->preconditioner, target, iterations, relres, &conv);
+    if (!rc && mem != FL_MEM_DEVICE && z.n > 0) {
+        cudaError_t e = cudaMemcpy(u, target, sizeof(double) * (size_t)z.n, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    du.release();
+    if (!rc && !conv)
+        return set_error(FL_E_MAX_ITER_EXCEEDED, "cg did not reach rel_tol in max_iter iterations");
+    return rc;
+}
+
 FL_API int fl_matvec(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr,
                      const int32_t* row_idx, const double* values, const double* x, double* y,
                      int mem) {

@@ -99,6 +99,11 @@ int cg_solve_device(fl_ctx* ctx, int32_t n, const int32_t* col_ptr, const int32_
                     const double* values, const double* b, double rel_tol, int64_t max_iter,
                     int precond, double* x_out, int64_t* iterations, double* relres, int32_t* converged);
 int scatter_free(fl_ctx* ctx, int32_t nf, const int32_t* free_nodes, const double* x, double* u);
+int solve_neumann_device(fl_ctx* ctx, int dim, int32_t n, int32_t nt, const double* nodes,
+                         const int32_t* elems, const int32_t* col_ptr, const int32_t* row_idx,
+                         const double* values, const double* b, int32_t pin, double rel_tol,
+                         int64_t max_iter, int precond, double* u, int64_t* iterations, double* relres,
+                         int32_t* converged);
 int launch_from_triplets(fl_ctx* ctx, int32_t m, int32_t n, int64_t nz, const int32_t* ii,
                          const int32_t* jj, const double* ss, fl_result* res);
 int matvec_device(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,

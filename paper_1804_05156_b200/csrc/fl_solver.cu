@@ -331,6 +331,185 @@ int cg_solve_device(fl_ctx* ctx, int32_t n, const int32_t* col_ptr, const int32_
     return rc;
 }
 
+namespace {
+
+// A with row and column `pin` removed (indices above pin shift down by one)
+__global__ void k_drop_count(int32_t n, int32_t pin, const int32_t* __restrict__ col_ptr,
+                             const int32_t* __restrict__ row_idx, int32_t* __restrict__ cnt) {
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        if (c == pin) continue;
+        int32_t k = 0;
+        for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) k += row_idx[e] != pin;
+        cnt[c < pin ? c : c - 1] = k;
+    }
+}
+
+__global__ void k_drop_fill(int32_t n, int32_t pin, const int32_t* __restrict__ col_ptr,
+                            const int32_t* __restrict__ row_idx, const double* __restrict__ val,
+                            const int32_t* __restrict__ out_ptr, int32_t* __restrict__ out_row,
+                            double* __restrict__ out_val) {
+    for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        if (c == pin) continue;
+        int32_t o = out_ptr[c < pin ? c : c - 1];
+        for (int32_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+            const int32_t r = row_idx[e];
+            if (r == pin) continue;
+            out_row[o] = r < pin ? r : r - 1;
+            out_val[o] = val[e];
+            ++o;
+        }
+    }
+}
+
+// b_r = (b - mean) without entry pin (enforce_compatibility, system.hpp:205-212)
+__global__ void k_drop_rhs(int32_t n, int32_t pin, const double* __restrict__ mean,
+                           const double* __restrict__ b, double* __restrict__ br) {
+    const double mu = *mean;
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        if (k != pin) br[k < pin ? k : k - 1] = __dsub_rn(b[k], mu);
+}
+
+// partial sums of b (the mean)
+__global__ void __launch_bounds__(kRed) k_sum_partial(int32_t n, const double* __restrict__ a,
+                                                      double* __restrict__ partial) {
+    __shared__ double sh[kRed / 32];
+    double v = 0.0;
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        v = __dadd_rn(v, a[k]);
+    const double t = block_sum(v, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_mean(int nb, const double* __restrict__ partial, double n, double* __restrict__ out) {
+    double t = 0.0;
+    for (int q = 0; q < nb; ++q) t = __dadd_rn(t, partial[q]);
+    *out = __ddiv_rn(t, n);
+}
+
+// u = x with 0 at pin
+__global__ void k_insert_pin(int32_t n, int32_t pin, const double* __restrict__ x, double* __restrict__ u) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        u[k] = k == pin ? 0.0 : x[k < pin ? k : k - 1];
+}
+
+// zero_average_shift (system.hpp:217-234): partials of sum avg(u)|t| and sum |t|
+template <int D>
+__global__ void __launch_bounds__(kRed) k_shift_partial(int32_t nt, const double* __restrict__ nodes,
+                                                        const int32_t* __restrict__ elems,
+                                                        const double* __restrict__ u,
+                                                        double* __restrict__ pw, double* __restrict__ pt) {
+    __shared__ double sh[kRed / 32];
+    double w = 0.0, tot = 0.0;
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        int32_t v[D + 1];
+        for (int k = 0; k <= D; ++k) v[k] = elems[(size_t)t * (D + 1) + k];
+        double meas;
+        if (D == 2) {  // mesh.hpp:34-38
+            const double* a = nodes + (size_t)v[0] * 2;
+            const double* b = nodes + (size_t)v[1] * 2;
+            const double* c = nodes + (size_t)v[2] * 2;
+            meas = fabs(__dmul_rn(0.5, __dsub_rn(__dmul_rn(__dsub_rn(b[0], a[0]), __dsub_rn(c[1], a[1])),
+                                                 __dmul_rn(__dsub_rn(c[0], a[0]), __dsub_rn(b[1], a[1])))));
+        } else {  // mesh.hpp:42-51
+            const double* a = nodes + (size_t)v[0] * 3;
+            double e[3][3];
+            for (int k = 0; k < 3; ++k)
+                for (int x = 0; x < 3; ++x) e[k][x] = __dsub_rn(nodes[(size_t)v[k + 1] * 3 + x], a[x]);
+            const double cx = __dsub_rn(__dmul_rn(e[0][1], e[1][2]), __dmul_rn(e[0][2], e[1][1]));
+            const double cy = __dsub_rn(__dmul_rn(e[0][2], e[1][0]), __dmul_rn(e[0][0], e[1][2]));
+            const double cz = __dsub_rn(__dmul_rn(e[0][0], e[1][1]), __dmul_rn(e[0][1], e[1][0]));
+            meas = fabs(__ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, e[2][0]), __dmul_rn(cy, e[2][1])),
+                                            __dmul_rn(cz, e[2][2])), 6.0));
+        }
+        double avg = 0.0;
+        for (int k = 0; k <= D; ++k) avg = __dadd_rn(avg, u[v[k]]);
+        avg = __ddiv_rn(avg, (double)(D + 1));
+        w = __dadd_rn(w, __dmul_rn(avg, meas));
+        tot = __dadd_rn(tot, meas);
+    }
+    const double a = block_sum(w, sh);
+    const double b = block_sum(tot, sh);
+    if (threadIdx.x == 0) {
+        pw[blockIdx.x] = a;
+        pt[blockIdx.x] = b;
+    }
+}
+
+__global__ void k_shift(int32_t n, int nb, const double* __restrict__ pw, const double* __restrict__ pt,
+                        double* __restrict__ u) {
+    double w = 0.0, t = 0.0;
+    for (int q = 0; q < nb; ++q) {
+        w = __dadd_rn(w, pw[q]);
+        t = __dadd_rn(t, pt[q]);
+    }
+    const double c = __ddiv_rn(w, t);
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        u[k] = __dsub_rn(u[k], c);
+}
+
+}  // namespace
+
+// solve_poisson's pure-Neumann path (solver.hpp:254-276) on device arrays
+int solve_neumann_device(fl_ctx* ctx, int dim, int32_t n, int32_t nt, const double* nodes,
+                         const int32_t* elems, const int32_t* col_ptr, const int32_t* row_idx,
+                         const double* values, const double* b, int32_t pin, double rel_tol,
+                         int64_t max_iter, int precond, double* u, int64_t* iterations, double* relres,
+                         int32_t* converged) {
+    const cudaStream_t s = ctx->stream;
+    if (pin < 0 || pin >= n) return set_error(FL_E_INDEX_OUT_OF_RANGE, "pin_node out of range");
+    DevBuf cnt, ptr, row, val, br, x, part;
+    auto release = [&]() {
+        DevBuf* all[] = {&cnt, &ptr, &row, &val, &br, &x, &part};
+        for (DevBuf* d : all) d->release();
+    };
+    auto run = [&]() -> int {
+        const int32_t nr = n - 1;
+        const int g = std::max(1, std::min(div_up(n, 256), ctx->sm_count * 8));
+        FL_TRY(part.ensure(sizeof(double) * (2 * kRedBlocks + 2)));
+        double* pp = part.as<double>();
+        double* mean = pp + 2 * kRedBlocks;
+        const int rb = std::min(kRedBlocks, std::max(1, div_up(n, kRed)));
+        k_sum_partial<<<rb, kRed, 0, s>>>(n, b, pp);
+        k_mean<<<1, 1, 0, s>>>(rb, pp, (double)n, mean);
+        FL_TRY(cnt.ensure(sizeof(int32_t) * ((size_t)nr + 1)));
+        FL_TRY(ptr.ensure(sizeof(int32_t) * ((size_t)nr + 2)));
+        FL_TRY(br.ensure(sizeof(double) * (size_t)std::max(nr, 1)));
+        FL_TRY(x.ensure(sizeof(double) * (size_t)std::max(nr, 1)));
+        k_drop_count<<<g, 256, 0, s>>>(n, pin, col_ptr, row_idx, cnt.as<int32_t>());
+        k_drop_rhs<<<g, 256, 0, s>>>(n, pin, mean, b, br.as<double>());
+        count_launch(ctx, 4);
+        FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(nr)));
+        const int32_t* cc = cnt.as<int32_t>();
+        FL_CUDA(launch_scan<int32_t>(nr, [cc] __device__(int64_t i) { return (int64_t)cc[i]; },
+                                     ptr.as<int32_t>(), ctx->scan_ws.p, s));
+        count_launch(ctx);
+        int32_t* h = reinterpret_cast<int32_t*>(static_cast<double*>(ctx->pinned) + 8);
+        FL_CUDA(cudaMemcpyAsync(h, ptr.as<int32_t>() + nr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        FL_CUDA(cudaStreamSynchronize(s));
+        const int64_t nnz = h[0];
+        FL_TRY(row.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
+        FL_TRY(val.ensure(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
+        k_drop_fill<<<g, 256, 0, s>>>(n, pin, col_ptr, row_idx, values, ptr.as<int32_t>(), row.as<int32_t>(),
+                                      val.as<double>());
+        count_launch(ctx);
+        FL_TRY(cg_solve_device(ctx, nr, ptr.as<int32_t>(), row.as<int32_t>(), val.as<double>(),
+                               br.as<double>(), rel_tol, max_iter, precond, x.as<double>(), iterations,
+                               relres, converged));
+        k_insert_pin<<<g, 256, 0, s>>>(n, pin, x.as<double>(), u);
+        const int rt = std::min(kRedBlocks, std::max(1, div_up(nt, kRed)));
+        if (dim == 2) k_shift_partial<2><<<rt, kRed, 0, s>>>(nt, nodes, elems, u, pp, pp + kRedBlocks);
+        else k_shift_partial<3><<<rt, kRed, 0, s>>>(nt, nodes, elems, u, pp, pp + kRedBlocks);
+        k_shift<<<g, 256, 0, s>>>(n, rt, pp, pp + kRedBlocks, u);
+        count_launch(ctx, 3);
+        FL_CUDA(cudaGetLastError());
+        return FL_OK;
+    };
+    const int rc = run();
+    cudaStreamSynchronize(s);
+    release();
+    return rc;
+}
+
 int scatter_free(fl_ctx* ctx, int32_t nf, const int32_t* free_nodes, const double* x, double* u) {
     if (nf > 0) {
         k_scatter_free<<<std::min(div_up(nf, 256), ctx->sm_count * 8), 256, 0, ctx->stream>>>(nf, free_nodes,
