@@ -442,6 +442,15 @@ __device__ __forceinline__ void lane_compute(const ColParams& p, Lane<D>& L, int
     const uint32_t key = __ldg(p.inc + p0 + k);
     L.t = (int32_t)(key & 0x3FFFFFFFu);
     L.j = (int)(key >> 30);
+    if (p.srec) {  // hybrid pass: the element records are already computed
+        const double* row = p.srec + ((size_t)L.t * (D + 1) + L.j) * 4;
+#pragma unroll
+        for (int i = 0; i <= D; ++i) L.s[i] = __ldg(row + i);
+        L.l = !p.want_b ? 0.0 : D == 3 ? __ldg(p.lrec + (size_t)L.t * 4 + L.j) : __ldg(row + 3);
+#pragma unroll
+        for (int i = 0; i <= D; ++i) L.R[i] = __ldg(p.elems + (size_t)L.t * (D + 1) + i);
+        return;
+    }
     if (D == 3) {
         const int4 q = __ldg(reinterpret_cast<const int4*>(p.elems) + L.t);
         L.R[0] = q.x;
