@@ -760,8 +760,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_columns(ColParams p) {
                 agg_a += (uint64_t)s_na[q];
                 agg_f += (uint64_t)s_nf[q];
             }
-            // packed [61:31] = A(free,free) count, [30:0] = A count
-            const uint64_t e = warp_lookback(p.tile_status, tile, (agg_f << 31) | agg_a);
+            uint64_t e;
+            if (p.col_list) {  // hybrid: any staging order will do (offsets are recorded)
+                e = 0;
+                if (threadIdx.x == 0) {
+                    const unsigned long long oa = atomicAdd(p.ov_alloc, (unsigned long long)agg_a);
+                    const unsigned long long of = atomicAdd(p.ov_alloc + 1, (unsigned long long)agg_f);
+                    e = (of << 31) | oa;
+                }
+            } else {
+                // packed [61:31] = A(free,free) count, [30:0] = A count
+                e = warp_lookback(p.tile_status, tile, (agg_f << 31) | agg_a);
+            }
             if (threadIdx.x == 0) s_off = e;
         }
         __syncthreads();
@@ -1016,16 +1026,28 @@ int launch_result_counts(fl_ctx* ctx, fl_result* res, int64_t* dev_out) {
 __global__ void k_list_big(int32_t n_cols, int32_t n_nodes, int dim, int lanes,
                            const int32_t* __restrict__ inc_ptr, int32_t* __restrict__ list,
                            int32_t* __restrict__ ovidx, unsigned long long* __restrict__ acc) {
-    for (int32_t lc = blockIdx.x * blockDim.x + threadIdx.x; lc < n_cols; lc += gridDim.x * blockDim.x) {
-        const int32_t m = inc_ptr[lc + 1] - inc_ptr[lc];
-        int32_t q = -1;
-        if (m > lanes) {
-            q = (int32_t)atomicAdd(acc, 1ull);
-            list[q] = lc;
-            const int64_t b = (int64_t)m * dim + 1;
-            atomicAdd(acc + 1, (unsigned long long)(b < n_nodes ? b : n_nodes));
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; base < n_cols; base += stride) {
+        const int32_t lc = (int32_t)(base + lane);
+        const int32_t m = lc < n_cols ? inc_ptr[lc + 1] - inc_ptr[lc] : 0;
+        const bool big = m > lanes;
+        const unsigned bal = __ballot_sync(0xffffffffu, big);  // one atomic per warp
+        int64_t bnd = big ? ((int64_t)m * dim + 1 < n_nodes ? (int64_t)m * dim + 1 : (int64_t)n_nodes) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bnd += __shfl_xor_sync(0xffffffffu, bnd, o);
+        int32_t q0 = 0;
+        if (lane == 0 && bal) {
+            q0 = (int32_t)atomicAdd(acc, (unsigned long long)__popc(bal));
+            atomicAdd(acc + 1, (unsigned long long)bnd);
         }
-        ovidx[lc] = q;
+        q0 = __shfl_sync(0xffffffffu, q0, 0);
+        int32_t q = -1;
+        if (big) {
+            q = q0 + __popc(bal & ((1u << lane) - 1));
+            list[q] = lc;
+        }
+        if (lc < n_cols) ovidx[lc] = q;
     }
 }
 
@@ -1107,11 +1129,11 @@ int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* 
     const int32_t NC = p.n_cols;
     // 1. the columns above the register kernel's valence, and their output bound
     FL_TRY(res->hyb[0].ensure(sizeof(int32_t) * 2 * ((size_t)NC + 1)));  // list | ovidx
-    FL_TRY(res->hyb[1].ensure(sizeof(unsigned long long) * 2));
+    FL_TRY(res->hyb[1].ensure(sizeof(unsigned long long) * 4));
     int32_t* list = res->hyb[0].as<int32_t>();
     int32_t* ovidx = list + NC + 1;
     unsigned long long* acc = res->hyb[1].as<unsigned long long>();
-    FL_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 2, s));
+    FL_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 4, s));
     k_list_big<<<std::max(1, std::min(div_up(NC, 256), ctx->sm_count * 8)), 256, 0, s>>>(
         NC, p.n_nodes, dim, lanes, p.inc_ptr, list, ovidx, acc);
     count_launch(ctx);
@@ -1137,6 +1159,7 @@ int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* 
     q.values = res->hyb[4].as<double>();
     q.ff_row_idx = res->hyb[5].as<int32_t>();
     q.ff_values = res->hyb[6].as<double>();
+    q.ov_alloc = acc + 2;
     q.cap_a = q.want_a ? bound : 0;
     q.cap_ff = q.want_sys ? bound : 0;
     if (n_list > 0) {

@@ -68,6 +68,7 @@ struct ColParams {
     int32_t n_list;
     int32_t* ov_cnt;
     int32_t* ov_off;
+    unsigned long long* ov_alloc;  // [2] running A / A(free,free) overflow-staging tops
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
