@@ -53,6 +53,7 @@ struct V3Smem {  // one per group
     uint4 msk[V3<D, L>::HS];                 // slot -> per-pass lane mask of its items
     int32_t srow[V3<D, L>::HS];              // rows in ascending order
     double sval[V3<D, L>::HS];
+    double stv[V3<D, L>::HS];                // lift: A(c, row) in row order, then A(c,row) u0[row]
     alignas(16) double lb[L];                // load shares in lane order
     alignas(16) double ld[L];                // s_jj in lane order
     double itm[D + 1][L];                    // item (i, lane) = s_i of the lane's element
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
     }
 }
 
-template <int D, int L, bool PRE>
+template <int D, int L, bool PRE, bool LIFT>
 __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3(ColParams p) {
     using C = V3<D, L>;
     constexpr int NV = D + 1;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
             }
             const double b = __shfl_sync(FULL, fold, 0, L);
             const double dg = __shfl_sync(FULL, fold, 1, L);
+            double ylift = 0.0;  // (A u0)[c], lift path (group lane 0)
             // ---- 4. off-diagonal items.  Item (i, lane) sits at itm[i][lane]; its
             //      row's slot (CAS insert) gets the lane's bit in msk[slot][i].
             //      Slot h then folds its items pass by pass, lanes ascending: the
@@ -367,12 +369,17 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 }
                 __syncwarp();
                 const int n4 = (nocc + 3) >> 2;
+                unsigned jm[NV];  // lift: lanes (group-relative) whose incidence has j == jj
+#pragma unroll
+                for (int jj = 0; jj < NV; ++jj)
+                    jm[jj] = LIFT ? (__ballot_sync(FULL, valid && j == jj) & gmask) >> (gi * L) : 0u;
 #pragma unroll
                 for (int base = 0; base < C::HS; base += L) {
                     const int h = base + g;
                     const int32_t r = sm.row[h];
                     if (r >= 0) {
                         double acc = dg;
+                        double tacc = dg;  // A(c, r): the transposed entry (lift only)
                         if (r != c) {
                             acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
                             // bit b of the concatenated pass masks = item itm[b / L][b % L]:
@@ -390,6 +397,19 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                                                     ((uint64_t)mk4.z << (2 * L));
                                 for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
                             }
+                            if constexpr (LIFT) {
+                                // A(c, r) folds the same items in (i_c*(d+1)+j_r, t) order: the
+                                // lane's own j (lanes are sorted by j: contiguous ranges jm[jj])
+                                // first, then the pass, then lanes ascending
+                                tacc = -0.0;
+                                const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+#pragma unroll
+                                for (int jj = 0; jj < NV; ++jj)
+#pragma unroll
+                                    for (int i = 0; i < NV; ++i)
+                                        for (unsigned mm = mk[i] & jm[jj]; mm; mm &= mm - 1)
+                                            tacc = tacc + sm.itm[i][__ffs(mm) - 1];
+                            }
                         }
                         int rk = 0;  // rows below r; unused entries (-1) compare as huge
                         const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
@@ -401,6 +421,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                         if (rk < C::MAXS) {
                             sm.srow[rk] = r;
                             sm.sval[rk] = acc;
+                            sm.stv[rk] = tacc;
                         }
                     }
                 }
@@ -410,6 +431,32 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 }
                 const int nslot = nocc;
                 __syncwarp();
+                if constexpr (LIFT) {
+                    // y = (A u0)[c] = 0.0 + A(c, r) * u0[r] over the stored entries of row c,
+                    // r ascending (matvec, sparse.hpp:129-141); u0 = g at Dirichlet nodes
+                    uint32_t umask = 0;  // rows whose product enters the sum
+                    for (int base = 0; base < C::MAXS; base += L) {
+                        const int q = base + g;
+                        bool use = false;
+                        if (q < nslot) {
+                            const double a = sm.stv[q];
+                            const int32_t r = sm.srow[q];
+                            if (a != 0.0 && p.is_dir[r]) {
+                                const double u = node_field3(p.g_dir, p.nodes, D, r);
+                                use = u != 0.0;
+                                sm.stv[q] = a * u;
+                            }
+                        }
+                        umask |= ((__ballot_sync(FULL, use) & gmask) >> (gi * L)) << base;
+                    }
+                    __syncwarp();
+                    if (g == 0) {
+                        double yy = 0.0;
+                        for (uint32_t mm = umask; mm; mm &= mm - 1) yy = yy + sm.stv[__ffs(mm) - 1];
+                        ylift = yy;
+                    }
+                    __syncwarp();
+                }
                 const bool col_free = act && p.want_sys && __ldg(p.fidx + c) >= 0;
                 int na = 0, nf = 0;
                 // compaction in chunks of L entries; pass 1: counts per group (one
@@ -483,7 +530,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 if (p.want_b) p.b[lc] = b;
                 if (p.want_sys) {
                     const double u0 = p.is_dir[c] ? node_field3(p.g_dir, p.nodes, D, c) : 0.0;
-                    const double bmod = b - 0.0;  // no lift on this path (g == 0)
+                    const double bmod = LIFT ? b - ylift : b - 0.0;  // system.hpp:197-198
                     p.u0[lc] = u0;
                     p.b_mod[lc] = bmod;
                     const int32_t fc = p.fidx[c];
@@ -499,7 +546,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
     }
 }
 
-template <int D, int L, bool PRE>
+template <int D, int L, bool PRE, bool LIFT>
 static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
     using C = V3<D, L>;
     FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
@@ -520,30 +567,36 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
         }
     }
     int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE>,
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE, LIFT>,
                                                           C::WARPS * 32, 0));
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS,
                              (int64_t)ctx->sm_count * std::max(per_sm, 1)));
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
-    k_columns3<D, L, PRE><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
+    k_columns3<D, L, PRE, LIFT><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
     return finish ? finish_staging(ctx, p, C::WTC) : FL_OK;
 }
 
-// kmax: the plan's largest node valence; need_lift meshes use the tiled kernel.
+// kmax: the plan's largest node valence; the lift (nonzero Dirichlet data) is a template branch.
 // pre: element-first records (default) or per-incidence geometry in the kernel.
 int columns3_lanes(int dim, int kmax) { return dim == 2 ? (kmax <= 8 ? 8 : 16) : 32; }
 
+template <int D, int L>
+static int launch3_sel(fl_ctx* ctx, ColParams& p, fl_result* res, bool pre, bool finish) {
+    if (!pre) return launch3<D, L, false, false>(ctx, p, res, finish);  // no lift (routed to v2)
+    return p.need_lift ? launch3<D, L, true, true>(ctx, p, res, finish)
+                       : launch3<D, L, true, false>(ctx, p, res, finish);
+}
+
 int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre, bool finish) {
     if (dim == 2) {
-        if (kmax <= 8)
-            return pre ? launch3<2, 8, true>(ctx, p, res, finish) : launch3<2, 8, false>(ctx, p, res, finish);
-        return pre ? launch3<2, 16, true>(ctx, p, res, finish) : launch3<2, 16, false>(ctx, p, res, finish);
+        if (kmax <= 8) return launch3_sel<2, 8>(ctx, p, res, pre, finish);
+        return launch3_sel<2, 16>(ctx, p, res, pre, finish);
     }
-    return pre ? launch3<3, 32, true>(ctx, p, res, finish) : launch3<3, 32, false>(ctx, p, res, finish);
+    return launch3_sel<3, 32>(ctx, p, res, pre, finish);
 }
 
 }  // namespace fl
