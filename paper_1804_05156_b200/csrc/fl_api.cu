@@ -602,13 +602,16 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             if (k == '1') {
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
-            } else if (k == '2' || (p.need_lift && k == '3') ||
-                       (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)) {
+            } else if (k == '2' || (k == '3' && (p.need_lift || (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)))) {
                 FL_TRY(launch_columns2(ctx, mesh->dim, p, mesh->max_inc, res));
-            } else if (mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc)) {
-                FL_TRY(launch_hybrid(ctx, mesh->dim, p, mesh, res, k != '3'));
             } else {
-                FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res, k != '3'));
+                // Neumann data: per-node shares first, added by the register kernel
+                if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)
+                    FL_TRY(launch_neumann_add(ctx, mesh->dim, p, res));
+                if (mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc))
+                    FL_TRY(launch_hybrid(ctx, mesh->dim, p, mesh, res, k != '3'));
+                else
+                    FL_TRY(launch_columns3(ctx, mesh->dim, p, mesh->max_inc, res, k != '3'));
             }
         }
     }

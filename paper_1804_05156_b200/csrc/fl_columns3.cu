@@ -309,8 +309,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 }
                 if (m & 1) fold = fold + src[m - 1];
             }
-            const double b = __shfl_sync(FULL, fold, 0, L);
+            double b = __shfl_sync(FULL, fold, 0, L);
             const double dg = __shfl_sync(FULL, fold, 1, L);
+            if (p.nadd && act && p.is_neu[c]) b = b + p.nadd[lc];  // apply_neumann: b + add
             double ylift = 0.0;  // (A u0)[c], lift path (group lane 0)
             // ---- 4. off-diagonal items.  Item (i, lane) sits at itm[i][lane]; its
             //      row's slot (CAS insert) gets the lane's bit in msk[slot][i].

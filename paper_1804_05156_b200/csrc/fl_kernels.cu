@@ -449,6 +449,7 @@ __device__ __forceinline__ void lane_compute(const ColParams& p, Lane<D>& L, int
         L.l = !p.want_b ? 0.0 : D == 3 ? __ldg(p.lrec + (size_t)L.t * 4 + L.j) : __ldg(row + 3);
 #pragma unroll
         for (int i = 0; i <= D; ++i) L.R[i] = __ldg(p.elems + (size_t)L.t * (D + 1) + i);
+        if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE) ec.load(p.nodes, L.R);
         return;
     }
     if (D == 3) {
@@ -1200,6 +1201,84 @@ int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* 
         r, tc, ovidx, pf, q.row_idx, q.values, q.ff_row_idx, q.ff_values);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Neumann shares for the register kernel (apply_neumann, system.hpp:123-172):
+// add[c] = 0.0 + the shares of the flag-2 faces containing node c in face-major
+// (lf, t) order; the register kernel then forms b[c] + add[c].  Warp per node on
+// a flag-2 face.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32) k_neumann_add(ColParams p, double* __restrict__ add_out) {
+    const unsigned FULL = 0xffffffffu;
+    __shared__ uint32_t skey[kWarps][kMaxNeu];
+    __shared__ double sval[kWarps][kMaxNeu];
+    __shared__ int scnt[kWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const Recip R3 = recip(3.0);
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t lc64 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; lc64 < p.n_cols; lc64 += nw) {
+        const int32_t lc = (int32_t)lc64, c = p.c_begin + lc;
+        if (!p.is_neu[c]) continue;  // warp-uniform
+        if (lane == 0) scnt[w] = 0;
+        __syncwarp();
+        const int32_t p0 = p.inc_ptr[lc], m = p.inc_ptr[lc + 1] - p0;
+        for (int base = 0; base < m; base += 32) {
+            if (base + lane < m) {
+                const uint32_t key = __ldg(p.inc + p0 + base + lane);
+                const int32_t t = (int32_t)(key & 0x3FFFFFFFu);
+                const int j = (int)(key >> 30);
+                int32_t R[D + 1];
+#pragma unroll
+                for (int i = 0; i <= D; ++i) R[i] = __ldg(p.elems + (size_t)t * (D + 1) + i);
+                ElemCol<D> ec;
+                ec.load(p.nodes, R);
+                for (int lf = 0; lf <= D; ++lf) {
+                    if (lf == j || p.flags[(size_t)t * (D + 1) + lf] != 2) continue;
+                    const int q = atomicAdd(&scnt[w], 1);
+                    if (q < kMaxNeu) {
+                        skey[w][q] = ((uint32_t)lf << 30) | (uint32_t)t;
+                        sval[w][q] = ec.face_share(lf, p.g_neu, R3, t);
+                    } else {
+                        atomicOr(p.err, DERR_OVERFLOW);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {  // face-major (lf, t) order (mesh.hpp:222-246), from 0.0
+            const int n = min(scnt[w], kMaxNeu);
+            double a = 0.0;
+            uint32_t last = 0;
+            bool first = true;
+            for (int r = 0; r < n; ++r) {
+                int best = -1;
+                for (int q = 0; q < n; ++q) {
+                    const uint32_t k2 = skey[w][q];
+                    if ((first || k2 > last) && (best < 0 || k2 < skey[w][best])) best = q;
+                }
+                last = skey[w][best];
+                first = false;
+                a = a + sval[w][best];
+            }
+            add_out[lc] = a;
+        }
+        __syncwarp(FULL);
+    }
+}
+
+int launch_neumann_add(fl_ctx* ctx, int dim, ColParams& p, fl_result* res) {
+    FL_TRY(res->hyb[8].ensure(sizeof(double) * ((size_t)p.n_cols + 1)));
+    double* add = res->hyb[8].as<double>();
+    const int64_t warps = std::min<int64_t>(std::max<int32_t>(p.n_cols, 1), (int64_t)ctx->sm_count * 64);
+    const int grid = (int)std::max<int64_t>(1, (warps + kWarps - 1) / kWarps);
+    if (dim == 2) k_neumann_add<2><<<grid, kWarps * 32, 0, ctx->stream>>>(p, add);
+    else k_neumann_add<3><<<grid, kWarps * 32, 0, ctx->stream>>>(p, add);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    p.nadd = add;
     return FL_OK;
 }
 

@@ -69,6 +69,7 @@ struct ColParams {
     int32_t* ov_cnt;
     int32_t* ov_off;
     unsigned long long* ov_alloc;  // [2] running A / A(free,free) overflow-staging tops
+    const double* nadd;  // Neumann shares per owned column (k_neumann_add), nullptr = none
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
@@ -89,6 +90,7 @@ int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res
 int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre,
                     bool finish = true);
 int columns3_lanes(int dim, int kmax);
+int launch_neumann_add(fl_ctx* ctx, int dim, ColParams& p, fl_result* res);
 int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* res, bool pre);
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
 int finish_staging(fl_ctx* ctx, ColParams& p, int tc);

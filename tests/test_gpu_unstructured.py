@@ -91,3 +91,19 @@ def test_unstructured_sharded_hybrid(world, ctx):
     np.testing.assert_array_equal(aff.col_ptr, ref.a_ff.col_ptr)
     assert aff.values.tobytes() == ref.a_ff.values.tobytes()
     assert np.concatenate([p.vector(_lib.B_F) for p in parts]).tobytes() == ref.b_f.tobytes()
+
+
+@pytest.mark.parametrize("dim,npts,seed,cluster", [(2, 2000, 7, 400), (3, 800, 8, 300)])
+def test_unstructured_neumann_and_lift(dim, npts, seed, cluster, ctx, ref_which):
+    """Neumann shares + Dirichlet lift on a mesh with hybrid-pass columns."""
+    m = _delaunay(dim, npts, seed, cluster)
+    m = fl.set_boundary_flags(Mesh(m.dim, m.nodes, m.elems), fl.classifier_mixed)
+    ref = po.assemble_blockwise(m.dim, m.nodes, m.elems, which=ref_which)
+    b = po.assemble_load(m.dim, m.nodes, m.elems, po.FIELD_CONST, 1.0, which=ref_which)
+    bn = po.apply_neumann(m.dim, m.nodes, m.elems, m.bd_flags, b, po.FIELD_X, 0.0, which=ref_which)
+    u0, bm = po.apply_dirichlet(m.dim, m.nodes, m.elems, m.bd_flags, ref, bn, po.FIELD_X, 0.0,
+                                which=ref_which)
+    s = fl.poisson_system(m, 1.0, "x", g_neumann="x", ctx=ctx)
+    assert s.b.tobytes() == bn.tobytes()
+    assert s.b_mod.tobytes() == bm.tobytes()
+    assert s.a.values.tobytes() == ref.values.tobytes()
