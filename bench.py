@@ -205,7 +205,9 @@ def run_ours(args, rank: int, world: int):
     from paper_1804_05156_b200.mesh import DeviceMesh
     from paper_1804_05156_b200.shard import column_ranges
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; FL_BENCH_BACKEND=gloo is a functional check of the
+    # sharded path on fewer GPUs (ranks share a device; its numbers mean nothing)
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     L = _lib.lib()
     ctx = fl.Context(dev)
@@ -237,15 +239,15 @@ def run_ours(args, rank: int, world: int):
         ff.mem, ff.samples = _lib.MEM_DEVICE, f_dev.data_ptr()
 
     counts = torch.zeros(4, dtype=torch.int64, device=f"cuda:{dev}")
-    all_counts = torch.zeros(world * 4, dtype=torch.int64, device=f"cuda:{dev}")
+    all_counts = [torch.zeros(4, dtype=torch.int64, device=f"cuda:{dev}") for _ in range(world)]
 
     def step():
         _lib.check(L.fl_assemble(ctx.handle, dm.handle, C.byref(ff), C.byref(fc), C.byref(fd),
                                  C.byref(fn), what, res.handle), "fl_assemble")
         if world > 1:  # the nnz-offset exchange (NCCL all_gather on the same stream)
             _lib.check(L.fl_result_counts_async(res.handle, counts.data_ptr()))
-            dist.all_gather_into_tensor(all_counts, counts)
-            torch.cumsum(all_counts.view(world, 4), dim=0)
+            dist.all_gather(all_counts, counts)
+            torch.cumsum(torch.stack(all_counts), dim=0)
 
     flush = None
     ws_bytes = configs.system_bytes(d, N, NT, 0, 0, 0)
@@ -287,7 +289,7 @@ def run_ours(args, rank: int, world: int):
         t = torch.tensor([ms_local], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        gathered = all_counts.view(world, 4).cpu().numpy()
+        gathered = torch.stack(all_counts).cpu().numpy()
     col_ms = float(np.mean([p[2] for p in phase]))
     plan_ms = float(np.mean([p[0] for p in phase]))
     mark_ms = float(np.mean([p[1] for p in phase]))
@@ -468,7 +470,7 @@ def main():
         log("[bench] warning: fewer than 3 warm-up steps")
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("FL_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         run_reference_impl(args, rank, world)
         return
