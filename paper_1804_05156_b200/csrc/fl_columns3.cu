@@ -35,29 +35,35 @@
 
 namespace fl {
 
-template <int D, int L>
+__host__ __device__ constexpr int lg2(int x) { return x <= 1 ? 0 : 1 + lg2(x >> 1); }
+
+// K incidences per lane: K = 2 (3-D) takes columns of up to 64 incidences
+template <int D, int L, int K = 1>
 struct V3 {
     static constexpr int NV = D + 1;
     static constexpr int GPW = 32 / L;                 // column groups per warp
-    static constexpr int HS = D == 2 ? 16 : 32;        // slot table entries per group
-    static constexpr int MAXS = D == 2 ? 12 : 24;      // distinct rows accepted per column
+    static constexpr int HS = D == 2 ? 16 : 32 * K;    // slot table entries per group
+    static constexpr int MAXS = D == 2 ? 12 : 24 * K;  // distinct rows accepted per column
     static constexpr int WTC = D == 2 ? 32 : 8;        // columns per warp tile
     static constexpr int ITERS = WTC / GPW;            // group iterations per warp tile
     static constexpr int WARPS = 4;                    // warps per CTA
 };
 
-template <int D, int L>
+template <int D, int L, int K = 1>
 struct V3Smem {  // one per group
-    alignas(16) int32_t row[V3<D, L>::HS];  // slot -> row (-1 empty)
-    alignas(16) int32_t crow[V3<D, L>::HS];  // occupied rows, compacted (-1 padded)
-    uint4 msk[V3<D, L>::HS];                 // slot -> per-pass lane mask of its items
-    int32_t srow[V3<D, L>::HS];              // rows in ascending order
-    double sval[V3<D, L>::HS];
-    double stv[V3<D, L>::HS];                // lift: A(c, row) in row order, then A(c,row) u0[row]
-    alignas(16) double lb[L];                // load shares in lane order
-    alignas(16) double ld[L];                // s_jj in lane order
-    double itm[D + 1][L];                    // item (i, lane) = s_i of the lane's element
+    using C = V3<D, L, K>;
+    alignas(16) int32_t row[C::HS];   // slot -> row (-1 empty)
+    alignas(16) int32_t crow[C::HS];  // occupied rows, compacted (-1 padded)
+    uint4 msk[C::HS][K];              // slot -> lane mask of its items, word [kk].(pass)
+    int32_t srow[C::HS];              // rows in ascending order
+    double sval[C::HS];
+    double stv[C::HS];                // lift: A(c, row) in row order, then A(c,row) u0[row]
+    alignas(16) double lb[L * K];     // load shares in incidence order
+    alignas(16) double ld[L * K];     // s_jj in incidence order
+    double itm[D + 1][L * K];         // item (i, incidence) = s_i of the incidence's element
 };
+
+__device__ __forceinline__ unsigned& mword(uint4& w, int i) { return reinterpret_cast<unsigned*>(&w)[i]; }
 
 __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* nodes, int dim,
                                               int32_t k) {
@@ -156,17 +162,18 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
     }
 }
 
-template <int D, int L, bool PRE, bool LIFT>
-__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3(ColParams p) {
-    using C = V3<D, L>;
+template <int D, int L, bool PRE, bool LIFT, int K>
+__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : 6) : 5) k_columns3(ColParams p) {
+    using C = V3<D, L, K>;
     constexpr int NV = D + 1;
+    constexpr int LK = L * K;  // incidences a group takes
     constexpr unsigned FULL = 0xffffffffu;
-    __shared__ V3Smem<D, L> sm_all[C::WARPS * C::GPW];
+    __shared__ V3Smem<D, L, K> sm_all[C::WARPS * C::GPW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gi = lane / L, g = lane % L;  // group in warp, lane in group
     const unsigned gmask = (L == 32) ? FULL : (((1u << L) - 1) << (gi * L));
     const unsigned lower = (1u << lane) - 1;
-    V3Smem<D, L>& sm = sm_all[warp * C::GPW + gi];
+    V3Smem<D, L, K>& sm = sm_all[warp * C::GPW + gi];
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
 
@@ -192,50 +199,89 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
         };
         int32_t p0n, mn;
         col_range(gi, p0n, mn);
-        uint32_t key_next = (g < mn && mn <= L) ? __ldg(p.inc + p0n + g) : 0xFFFFFFFFu;
+        uint32_t key_next[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+            key_next[kk] = (kk * L + g < mn && mn <= LK) ? __ldg(p.inc + p0n + kk * L + g) : 0xFFFFFFFFu;
         for (int it = 0; it < C::ITERS; ++it) {
             const int q = it * C::GPW + gi;
             const int32_t lc = lc0 + q;  // owned column
             const bool act = q < ncol_t;
             const int32_t c = p.c_begin + lc;  // global node
             int32_t m = mn;
-            uint32_t key = key_next;
+            uint32_t key[K];
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) key[kk] = key_next[kk];
             if (it + 1 < C::ITERS) {
                 col_range(q + C::GPW, p0n, mn);
-                key_next = (g < mn && mn <= L) ? __ldg(p.inc + p0n + g) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk)
+                    key_next[kk] = (kk * L + g < mn && mn <= LK) ? __ldg(p.inc + p0n + kk * L + g) : 0xFFFFFFFFu;
             }
-            if (m > L) {  // hybrid: the general kernel takes the column afterwards
+            if (m > LK) {  // hybrid: the general kernel takes the column afterwards
                 if (!p.hybrid) bad = true;
                 m = 0;
-                key = 0xFFFFFFFFu;
-            }
-            // ---- 1. keys, sorted ascending inside the group
 #pragma unroll
-            for (int k = 2; k <= L; k <<= 1) {
+                for (int kk = 0; kk < K; ++kk) key[kk] = 0xFFFFFFFFu;
+            }
+            // ---- 1. keys, sorted ascending inside the group: incidence e = kk*L + g
+            //      (bitonic over L*K; distances >= L pair registers of one lane)
+#pragma unroll
+            for (int k = 2; k <= LK; k <<= 1) {
 #pragma unroll
                 for (int jj = k >> 1; jj > 0; jj >>= 1) {
-                    const uint32_t o = __shfl_xor_sync(FULL, key, jj, L);
-                    const bool up = (g & k) == 0;
-                    const bool lo = (g & jj) == 0;
-                    key = (lo == up) ? min(key, o) : max(key, o);
+                    if (jj >= L) {
+#pragma unroll
+                        for (int kk = 0; kk < K; ++kk) {
+                            const int pk = kk ^ (jj / L);
+                            if (pk > kk) {
+                                const bool up = ((kk * L + g) & k) == 0;
+                                const uint32_t a = key[kk], b2 = key[pk];
+                                key[kk] = up ? min(a, b2) : max(a, b2);
+                                key[pk] = up ? max(a, b2) : min(a, b2);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < K; ++kk) {
+                            const uint32_t o = __shfl_xor_sync(FULL, key[kk], jj, L);
+                            const bool up = ((kk * L + g) & k) == 0;
+                            const bool lo = (g & jj) == 0;
+                            key[kk] = (lo == up) ? min(key[kk], o) : max(key[kk], o);
+                        }
+                    }
                 }
             }
-            const bool valid = g < m;
-            const int32_t t = (int32_t)(key & 0x3FFFFFFFu);
-            const int j = valid ? (int)(key >> 30) : 0;
+            bool valid[K];
+            int32_t t[K];
+            int j[K];
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                valid[kk] = kk * L + g < m;
+                t[kk] = (int32_t)(key[kk] & 0x3FFFFFFFu);
+                j[kk] = valid[kk] ? (int)(key[kk] >> 30) : 0;
+            }
             // ---- 2. geometry of column j of element t
-            int32_t R[NV];
-            double s[NV];
+            int32_t RR[K][NV];
+            double ss[K][NV];
+            double ll[K], sjjk[K];
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+            int32_t* R = RR[kk];
+            double* s = ss[kk];
             double l = 0.0, sjj = 0.0;
+            const int32_t t_ = t[kk];
+            const int j_ = j[kk];
+            const bool valid_ = valid[kk];
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 R[i] = -1;
                 s[i] = 0.0;
             }
-            if (valid && PRE) {
+            if (valid_ && PRE) {
                 // row j of the element's local matrix: one 256-bit load; the load
                 // share (3-D) and the vertex ids from their own arrays
-                const double* row = p.srec + ((size_t)t * NV + j) * 4;
+                const double* row = p.srec + ((size_t)t_ * NV + j_) * 4;
                 double q0, q1, q2, q3;
                 asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
                     : "=d"(q0), "=d"(q1), "=d"(q2), "=d"(q3) : "l"(row));
@@ -244,8 +290,8 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 s[2] = q2;
                 if constexpr (D == 3) {
                     s[3] = q3;
-                    l = __ldg(p.lrec + (size_t)t * 4 + j);
-                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
+                    l = __ldg(p.lrec + (size_t)t_ * 4 + j_);
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t_);
                     R[0] = e.x;
                     R[1] = e.y;
                     R[2] = e.z;
@@ -253,48 +299,55 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 } else {
                     l = q3;
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t * NV + i);
+                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t_ * NV + i);
                 }
-            } else if (valid) {
+            } else if (valid_) {
                 if constexpr (D == 3) {
-                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t);
+                    const int4 e = __ldg(reinterpret_cast<const int4*>(p.elems) + t_);
                     R[0] = e.x;
                     R[1] = e.y;
                     R[2] = e.z;
                     R[3] = e.w;
                 } else {
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t * NV + i);
+                    for (int i = 0; i < NV; ++i) R[i] = __ldg(p.elems + (size_t)t_ * NV + i);
                 }
                 {
                     ElemCol<D> ec;
                     ec.load(p.nodes, R);
                     double meas;
-                    if constexpr (D == 2) meas = ec.stiffness_col(j, s);
-                    else meas = ec.stiffness_col(j, s, R6);
+                    if constexpr (D == 2) meas = ec.stiffness_col(j_, s);
+                    else meas = ec.stiffness_col(j_, s, R6);
                     if (meas == 0.0) atomicOr(p.err, DERR_DEGENERATE);
                     if (p.want_a && p.coef.kind != FL_FIELD_NONE) {
                         double a;
                         if (p.coef.kind == FL_FIELD_CONST) a = p.coef.value;
-                        else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t);
+                        else if (p.coef.kind == FL_FIELD_SAMPLES) a = __ldg(p.coef.samples + t_);
                         else a = ec.coef_c5(R3);
 #pragma unroll
                         for (int i = 0; i < NV; ++i) s[i] = s[i] * a;
                     }
                     if (p.want_b) {
-                        if constexpr (D == 2) l = ec.load_col(j, t, p.f, R6);
-                        else l = ec.load_col(j, t, meas, p.f);
+                        if constexpr (D == 2) l = ec.load_col(j_, t_, p.f, R6);
+                        else l = ec.load_col(j_, t_, meas, p.f);
                     }
                 }
             }
-            if (valid) {
+            if (valid_) {
 #pragma unroll
                 for (int i = 0; i < NV; ++i)
-                    if (i == j) sjj = s[i];
+                    if (i == j_) sjj = s[i];
             }
+            ll[kk] = l;
+            sjjk[kk] = sjj;
+            }
+
             // ---- 3. b and the diagonal: sequential folds in lane order (lanes 0 / 1)
-            sm.lb[g] = l;
-            sm.ld[g] = sjj;
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) {
+                sm.lb[kk * L + g] = ll[kk];
+                sm.ld[kk * L + g] = sjjk[kk];
+            }
             __syncwarp();
             double fold = g == 0 ? 0.0 : -0.0;
             if (g < 2) {
@@ -321,19 +374,24 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 for (int h = g; h < C::HS; h += L) {
                     sm.row[h] = -1;
                     sm.crow[h] = -1;
-                    sm.msk[h] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk) sm.msk[h][kk] = make_uint4(0u, 0u, 0u, 0u);
                 }
 #pragma unroll
-                for (int i = 0; i < NV; ++i) sm.itm[i][g] = s[i];
+                for (int kk = 0; kk < K; ++kk)
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) sm.itm[i][kk * L + g] = ss[kk][i];
                 __syncwarp();
 #pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    if (!valid || i == j) continue;
+                for (int i = 0; i < NV; ++i)
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    if (!valid[kk] || i == j[kk]) continue;
                     // every lane inserts its own row (equal rows meet on one slot: the
                     // CAS returns the row) and sets its bit in the slot's pass-i mask;
                     // the bit position is the lane, so atomic order does not matter
-                    const int32_t r = R[i];
-                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                    const int32_t r = RR[kk][i];
+                    uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - lg2(C::HS));
                     int slot = -1;
                     for (int probe = 0; probe < C::HS; ++probe) {
                         const int32_t old = atomicCAS(&sm.row[h], -1, r);
@@ -343,13 +401,13 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                         }
                         h = (h + 1) & (C::HS - 1);
                     }
-                    if (slot >= 0) atomicOr(reinterpret_cast<unsigned*>(&sm.msk[slot]) + i, 1u << g);
+                    if (slot >= 0) atomicOr(&mword(sm.msk[slot][kk], i), 1u << g);
                     else bad = true;
                 }
                 __syncwarp();
                 // ---- 5. the diagonal slot, the folds, rows ranked, zero drop
                 if (g == 0 && act && m > 0) {
-                    uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - (D == 2 ? 4 : 5));
+                    uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - lg2(C::HS));
                     for (int probe = 0; probe < C::HS; ++probe) {
                         if (sm.row[h] == -1) {
                             sm.row[h] = c;
@@ -370,10 +428,12 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                 }
                 __syncwarp();
                 const int n4 = (nocc + 3) >> 2;
-                unsigned jm[NV];  // lift: lanes (group-relative) whose incidence has j == jj
+                unsigned jm[NV][K];  // lift: lanes (group-relative) whose incidence has j == jj
 #pragma unroll
                 for (int jj = 0; jj < NV; ++jj)
-                    jm[jj] = LIFT ? (__ballot_sync(FULL, valid && j == jj) & gmask) >> (gi * L) : 0u;
+#pragma unroll
+                    for (int kk = 0; kk < K; ++kk)
+                        jm[jj][kk] = LIFT ? (__ballot_sync(FULL, valid[kk] && j[kk] == jj) & gmask) >> (gi * L) : 0u;
 #pragma unroll
                 for (int base = 0; base < C::HS; base += L) {
                     const int h = base + g;
@@ -385,13 +445,14 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                             acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
                             // bit b of the concatenated pass masks = item itm[b / L][b % L]:
                             // ascending bits walk (i, lane) in the reference's order
-                            const uint4 mk4 = sm.msk[h];
-                            if constexpr (L == 32) {  // pass by pass, lanes ascending
-                                const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+                            const uint4 mk4 = sm.msk[h][0];
+                            if constexpr (L == 32) {  // pass by pass, incidences ascending
 #pragma unroll
                                 for (int i = 0; i < NV; ++i)
-                                    for (unsigned mm = mk[i]; mm; mm &= mm - 1)
-                                        acc = acc + sm.itm[i][__ffs(mm) - 1];
+#pragma unroll
+                                    for (int kk = 0; kk < K; ++kk)
+                                        for (unsigned mm = mword(sm.msk[h][kk], i); mm; mm &= mm - 1)
+                                            acc = acc + sm.itm[i][kk * L + __ffs(mm) - 1];
                             } else {  // the passes' L-bit masks concatenated: bit b = itm[b / L][b % L]
                                 const double* flat = &sm.itm[0][0];
                                 const uint64_t w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) |
@@ -403,13 +464,15 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
                                 // lane's own j (lanes are sorted by j: contiguous ranges jm[jj])
                                 // first, then the pass, then lanes ascending
                                 tacc = -0.0;
-                                const unsigned mk[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
 #pragma unroll
                                 for (int jj = 0; jj < NV; ++jj)
 #pragma unroll
                                     for (int i = 0; i < NV; ++i)
-                                        for (unsigned mm = mk[i] & jm[jj]; mm; mm &= mm - 1)
-                                            tacc = tacc + sm.itm[i][__ffs(mm) - 1];
+#pragma unroll
+                                        for (int kk = 0; kk < K; ++kk)
+                                            for (unsigned mm = mword(sm.msk[h][kk], i) & jm[jj][kk]; mm;
+                                                 mm &= mm - 1)
+                                                tacc = tacc + sm.itm[i][kk * L + __ffs(mm) - 1];
                             }
                         }
                         int rk = 0;  // rows below r; unused entries (-1) compare as huge
@@ -547,9 +610,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? 10 : 5) k_columns3
     }
 }
 
-template <int D, int L, bool PRE, bool LIFT>
+template <int D, int L, bool PRE, bool LIFT, int K>
 static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
-    using C = V3<D, L>;
+    using C = V3<D, L, K>;
     FL_TRY(prepare_staging(ctx, p, res, C::WTC, (int64_t)C::WTC * C::MAXS));
     if (ctx->profile) {
         FL_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
@@ -568,13 +631,13 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
         }
     }
     int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE, LIFT>,
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE, LIFT, K>,
                                                           C::WARPS * 32, 0));
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS,
                              (int64_t)ctx->sm_count * std::max(per_sm, 1)));
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
-    k_columns3<D, L, PRE, LIFT><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
+    k_columns3<D, L, PRE, LIFT, K><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
@@ -583,21 +646,25 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
 
 // kmax: the plan's largest node valence; the lift (nonzero Dirichlet data) is a template branch.
 // pre: element-first records (default) or per-incidence geometry in the kernel.
-int columns3_lanes(int dim, int kmax) { return dim == 2 ? (kmax <= 8 ? 8 : 16) : 32; }
+// incidences per column the register kernel takes (3-D: two per lane above 32)
+int columns3_lanes(int dim, int kmax) { return dim == 2 ? (kmax <= 8 ? 8 : 16) : (kmax <= 32 ? 32 : 64); }
 
-template <int D, int L>
+template <int D, int L, int K>
 static int launch3_sel(fl_ctx* ctx, ColParams& p, fl_result* res, bool pre, bool finish) {
-    if (!pre) return launch3<D, L, false, false>(ctx, p, res, finish);  // no lift (routed to v2)
-    return p.need_lift ? launch3<D, L, true, true>(ctx, p, res, finish)
-                       : launch3<D, L, true, false>(ctx, p, res, finish);
+    if constexpr (K == 1) {
+        if (!pre) return launch3<D, L, false, false, 1>(ctx, p, res, finish);  // no lift (routed to v2)
+    }
+    return p.need_lift ? launch3<D, L, true, true, K>(ctx, p, res, finish)
+                       : launch3<D, L, true, false, K>(ctx, p, res, finish);
 }
 
 int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre, bool finish) {
     if (dim == 2) {
-        if (kmax <= 8) return launch3_sel<2, 8>(ctx, p, res, pre, finish);
-        return launch3_sel<2, 16>(ctx, p, res, pre, finish);
+        if (kmax <= 8) return launch3_sel<2, 8, 1>(ctx, p, res, pre, finish);
+        return launch3_sel<2, 16, 1>(ctx, p, res, pre, finish);
     }
-    return launch3_sel<3, 32>(ctx, p, res, pre, finish);
+    if (kmax > 32 && pre) return launch3_sel<3, 32, 2>(ctx, p, res, pre, finish);
+    return launch3_sel<3, 32, 1>(ctx, p, res, pre, finish);
 }
 
 }  // namespace fl
