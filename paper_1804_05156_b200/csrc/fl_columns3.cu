@@ -42,8 +42,8 @@ template <int D, int L, int K = 1>
 struct V3 {
     static constexpr int NV = D + 1;
     static constexpr int GPW = 32 / L;                 // column groups per warp
-    static constexpr int HS = D == 2 ? 16 : 32 * K;    // slot table entries per group
-    static constexpr int MAXS = D == 2 ? 12 : 24 * K;  // distinct rows accepted per column
+    static constexpr int HS = D == 2 ? 16 : L * K;          // slot table entries per group
+    static constexpr int MAXS = D == 2 ? 12 : (3 * L * K) / 4;  // distinct rows accepted per column
     static constexpr int WTC = D == 2 ? 32 : 8;        // columns per warp tile
     static constexpr int ITERS = WTC / GPW;            // group iterations per warp tile
     static constexpr int WARPS = 4;                    // warps per CTA
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
 }
 
 template <int D, int L, bool PRE, bool LIFT, int K>
-__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : 6) : 5) k_columns3(ColParams p) {
+__global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L == 16 ? 8 : 6)) : 5) k_columns3(ColParams p) {
     using C = V3<D, L, K>;
     constexpr int NV = D + 1;
     constexpr int LK = L * K;  // incidences a group takes
@@ -386,7 +386,11 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : 6) 
                 for (int i = 0; i < NV; ++i)
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) {
-                    if (!valid[kk] || i == j[kk]) continue;
+                    // exact-zero items are skipped: x + (+-0) == x for x != 0, a zero
+                    // prefix only changes the sign of a zero that the next nonzero item
+                    // absorbs, and an entry whose items are all zero is dropped anyway
+                    // (sparse.hpp:105) -- so its row never needs a slot
+                    if (!valid[kk] || i == j[kk] || ss[kk][i] == 0.0) continue;
                     // every lane inserts its own row (equal rows meet on one slot: the
                     // CAS returns the row) and sets its bit in the slot's pass-i mask;
                     // the bit position is the lane, so atomic order does not matter
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : 6) 
                             // bit b of the concatenated pass masks = item itm[b / L][b % L]:
                             // ascending bits walk (i, lane) in the reference's order
                             const uint4 mk4 = sm.msk[h][0];
-                            if constexpr (L == 32) {  // pass by pass, incidences ascending
+                            if constexpr (D == 3) {  // pass by pass, incidences ascending
 #pragma unroll
                                 for (int i = 0; i < NV; ++i)
 #pragma unroll
