@@ -9,6 +9,7 @@
 #include "femlite_oracle.h"
 
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -849,5 +850,76 @@ int fo_coefficient_c5(int dim, int32_t n_elems, const double* nodes, const int32
         const double xbar = xs / (double)nv;
         coef_out[t] = 1.0 + 0.5 * sin((2.0 * M_PI) * xbar);
     }
+    return FO_OK;
+}
+
+/* ---- text writers ------------------------------------ */
+typedef struct {
+    char* p;
+    int64_t n, cap;
+} fo_buf;
+
+static void buf_put(fo_buf* b, const char* s, int64_t k) {
+    if (b->n + k + 1 > b->cap) {
+        b->cap = (b->n + k + 1) * 2;
+        b->p = (char*)realloc(b->p, (size_t)b->cap);
+    }
+    memcpy(b->p + b->n, s, (size_t)k);
+    b->n += k;
+}
+
+/* matrix_market.hpp:15-24: header, "m n nnz", then "row+1 col+1 %.17g" per
+ * entry, columns ascending */
+int fo_write_matrix_market(const fo_csc* a, char** text, int64_t* len) {
+    fo_buf b = {NULL, 0, 0};
+    char tmp[96];
+    int k = snprintf(tmp, sizeof tmp, "%%%%MatrixMarket matrix coordinate real general\n");
+    buf_put(&b, tmp, k);
+    k = snprintf(tmp, sizeof tmp, "%d %d %d\n", a->m, a->n, a->col_ptr[a->n]);
+    buf_put(&b, tmp, k);
+    for (int32_t c = 0; c < a->n; ++c)
+        for (int32_t q = a->col_ptr[c]; q < a->col_ptr[c + 1]; ++q) {
+            char v[32];
+            snprintf(v, sizeof v, "%.17g", a->values[q]);
+            k = snprintf(tmp, sizeof tmp, "%d %d %s\n", a->row_idx[q] + 1, c + 1, v);
+            buf_put(&b, tmp, k);
+        }
+    *text = b.p;
+    *len = b.n;
+    return FO_OK;
+}
+
+/* mesh_io.hpp:125-142: "d N NT", node coordinates ("%.17g", single spaces),
+ * one-based element vertices, flags as int */
+int fo_write_mesh(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                  const int32_t* elems, const int8_t* flags, char** text, int64_t* len) {
+    fo_buf b = {NULL, 0, 0};
+    char tmp[128];
+    const int nv = dim + 1;
+    int k = snprintf(tmp, sizeof tmp, "%d %d %d\n", dim, n_nodes, n_elems);
+    buf_put(&b, tmp, k);
+    for (int32_t q = 0; q < n_nodes; ++q) {
+        for (int c = 0; c < dim; ++c) {
+            k = snprintf(tmp, sizeof tmp, "%s%.17g", c ? " " : "", nodes[(size_t)q * dim + c]);
+            buf_put(&b, tmp, k);
+        }
+        buf_put(&b, "\n", 1);
+    }
+    for (int32_t t = 0; t < n_elems; ++t) {
+        for (int c = 0; c < nv; ++c) {
+            k = snprintf(tmp, sizeof tmp, "%s%d", c ? " " : "", elems[(size_t)t * nv + c] + 1);
+            buf_put(&b, tmp, k);
+        }
+        buf_put(&b, "\n", 1);
+    }
+    for (int32_t t = 0; t < n_elems; ++t) {
+        for (int c = 0; c < nv; ++c) {
+            k = snprintf(tmp, sizeof tmp, "%s%d", c ? " " : "", flags ? (int)flags[(size_t)t * nv + c] : 0);
+            buf_put(&b, tmp, k);
+        }
+        buf_put(&b, "\n", 1);
+    }
+    *text = b.p;
+    *len = b.n;
     return FO_OK;
 }

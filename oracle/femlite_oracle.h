@@ -107,6 +107,14 @@ int fo_apply_neumann(int dim, int32_t n_nodes, int32_t n_elems, const double* no
 int fo_coefficient_c5(int dim, int32_t n_elems, const double* nodes, const int32_t* elems,
                       double* coef_out);
 
+/* Text writers: the bytes of write_matrix_market
+ * (matrix_market.hpp:15-24) and write_mesh (mesh_io.hpp:125-142), "%.17g" for
+ * every double (detail::format_real, mesh_io.hpp:56-60) and decimal integers,
+ * into a malloc'd buffer (*text, *len bytes; free with fo_free). */
+int fo_write_matrix_market(const fo_csc* a, char** text, int64_t* len);
+int fo_write_mesh(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                  const int32_t* elems, const int8_t* flags, char** text, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -435,3 +435,49 @@ def ref_solve_poisson(dim, nodes, elems, flags, f_kind, f_value, g_kind, g_value
                                C.c_double(rel_tol), _p(u, _f64p), C.byref(it), C.byref(rr),
                                C.byref(sec)), "ref")
     return u, it.value, rr.value, sec.value
+
+
+# ---------------------------------------------------------------------------
+# text writers
+# ---------------------------------------------------------------------------
+def _take_text(L, ptr, n, free) -> bytes:
+    free.argtypes = [C.c_void_p]
+    data = C.string_at(ptr, n) if n else b""
+    free(ptr)
+    return data
+
+
+def write_matrix_market(a: Csc, which: str = "oracle", timing: bool = False):
+    """matrix_market.hpp:15-24 -> bytes (timing=True: (bytes, seconds), ref only)."""
+    L = lib(which)
+    txt, n = C.c_void_p(), C.c_int64()
+    if which == "oracle":
+        s = _fo_from(a)
+        _check(L.fo_write_matrix_market(C.byref(s), C.byref(txt), C.byref(n)))
+        out = _take_text(L, txt, n.value, L.fo_free)
+        return (out, float("nan")) if timing else out
+    a_cp, a_ri, a_va = _arr_i32(a.col_ptr), _arr_i32(a.row_idx), _arr_f64(a.values)
+    sec = C.c_double()
+    _check(L.ref_write_matrix_market(C.c_int32(a.m), C.c_int32(a.n), _p(a_cp, _i32p), _p(a_ri, _i32p),
+                                     _p(a_va, _f64p), C.byref(txt), C.byref(n), C.byref(sec)), "ref")
+    out = _take_text(L, txt, n.value, L.ref_free)
+    return (out, sec.value) if timing else out
+
+
+def write_mesh(dim, nodes, elems, flags=None, which: str = "oracle", timing: bool = False):
+    """mesh_io.hpp:125-142 -> bytes (timing=True: (bytes, seconds), ref only)."""
+    L = lib(which)
+    nodes, elems = _arr_f64(nodes), _arr_i32(elems)
+    fl = _arr_i8(flags) if flags is not None else None
+    nn, ne = nodes.shape[0], elems.shape[0]
+    txt, n = C.c_void_p(), C.c_int64()
+    if which == "oracle":
+        _check(L.fo_write_mesh(C.c_int(dim), C.c_int32(nn), C.c_int32(ne), _p(nodes, _f64p),
+                               _p(elems, _i32p), _p(fl, _i8p), C.byref(txt), C.byref(n)))
+        out = _take_text(L, txt, n.value, L.fo_free)
+        return (out, float("nan")) if timing else out
+    sec = C.c_double()
+    _check(L.ref_write_mesh(C.c_int(dim), C.c_int32(nn), C.c_int32(ne), _p(nodes, _f64p), _p(elems, _i32p),
+                            _p(fl, _i8p), C.byref(txt), C.byref(n), C.byref(sec)), "ref")
+    out = _take_text(L, txt, n.value, L.ref_free)
+    return (out, sec.value) if timing else out

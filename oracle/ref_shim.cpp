@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numbers>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -397,6 +398,40 @@ int ref_solve_poisson(int dim, int32_t n_nodes, int32_t n_elems, const double* n
         std::memcpy(u_out, sol.u.data(), sizeof(double) * sol.u.size());
         *iterations = sol.iterations;
         *relres = sol.final_relres;
+    });
+}
+
+// ---- text writers (matrix_market.hpp:15-24, mesh_io.hpp:125-142) -----------
+static void export_text(const std::string& t, char** text, int64_t* len) {
+    *len = static_cast<int64_t>(t.size());
+    *text = static_cast<char*>(std::malloc(t.size() + 1));
+    std::memcpy(*text, t.data(), t.size());
+}
+
+int ref_write_matrix_market(int32_t m, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
+                            const double* values, char** text, int64_t* len, double* seconds) {
+    return guarded([&] {
+        const CscMatrix a = import_csc(m, n, col_ptr, row_idx, values);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::ostringstream os;
+        write_matrix_market(a, os);
+        const std::string t = os.str();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        export_text(t, text, len);
+    });
+}
+
+int ref_write_mesh(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                   const int32_t* elems, const int8_t* flags, char** text, int64_t* len,
+                   double* seconds) {
+    return guarded([&] {
+        const Mesh m = mesh_from(dim, n_nodes, n_elems, nodes, elems, flags);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::ostringstream os;
+        write_mesh(m, os);
+        const std::string t = os.str();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        export_text(t, text, len);
     });
 }
 

@@ -66,6 +66,14 @@ SIGNATURES = {
     "fl_host_sample": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _vp, _vp, C.c_int, C.c_int,
                                  C.c_double, _vp]),
     "fl_host_points": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _vp, _vp, C.c_int, _vp]),
+    "fl_text_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "fl_text_destroy": (C.c_int, [_vp]),
+    "fl_text_size": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "fl_text_copy": (C.c_int, [_vp, _vp, C.c_int64, C.c_int]),
+    "fl_text_device_ptr": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]),
+    "fl_write_matrix_market": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, C.c_int, _vp]),
+    "fl_write_mesh": (C.c_int, [_vp, _vp, _vp]),
+    "fl_format_reals": (C.c_int, [_vp, C.c_int64, _vp, C.c_int, C.c_uint32, _vp]),
 }
 
 
