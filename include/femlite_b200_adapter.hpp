@@ -13,6 +13,8 @@
 //                                                    A(free, free), b_f -- one fused pass)
 //   femlite_b200::submatrix(a, rows, cols)           sparse.hpp:159    submatrix
 //   femlite_b200::matvec / cg_solve / solve_poisson  sparse.hpp:129, solver.hpp:63, :223
+//   femlite_b200::write_matrix_market(a, out)        matrix_market.hpp:15 write_matrix_market
+//   femlite_b200::write_mesh(mesh, out)              mesh_io.hpp:125      write_mesh
 //
 // Include it after the femlite headers.  Errors are rethrown as
 // femlite::Error with the reference's ErrorCode (the ABI status is
@@ -24,6 +26,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -336,6 +339,42 @@ inline femlite::CscMatrix submatrix(const femlite::CscMatrix& a,
                        static_cast<int32_t>(cols.size()), cols.data(), FL_MEM_HOST, r.r),
           "fl_submatrix");
     return r.matrix(static_cast<femlite::index_t>(rows.size()));
+}
+
+namespace detail {
+struct TextHandle {
+    fl_text* t = nullptr;
+    explicit TextHandle(Context& ctx) { check(fl_text_create(ctx.get(), &t), "fl_text_create"); }
+    ~TextHandle() { fl_text_destroy(t); }
+    TextHandle(const TextHandle&) = delete;
+    TextHandle& operator=(const TextHandle&) = delete;
+    void write_to(std::ostream& out) const {
+        int64_t n = 0;
+        check(fl_text_size(t, &n), "fl_text_size");
+        std::string s(static_cast<std::size_t>(n), '\0');
+        check(fl_text_copy(t, s.data(), n, FL_MEM_HOST), "fl_text_copy");
+        out.write(s.data(), static_cast<std::streamsize>(n));
+    }
+};
+}  // namespace detail
+
+/// matrix_market.hpp:15-24: the same bytes, formatted on the GPU (exact %.17g)
+inline void write_matrix_market(const femlite::CscMatrix& a, std::ostream& out,
+                                Context& ctx = Context::default_context()) {
+    detail::TextHandle t(ctx);
+    check(fl_write_matrix_market(ctx.get(), a.m, a.n, a.col_ptr.data(), a.row_idx.data(),
+                                 a.values.data(), FL_MEM_HOST, t.t),
+          "fl_write_matrix_market");
+    t.write_to(out);
+}
+
+/// mesh_io.hpp:125-142: the same bytes, formatted on the GPU
+inline void write_mesh(const femlite::Mesh& mesh, std::ostream& out,
+                       Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::TextHandle t(ctx);
+    check(fl_write_mesh(ctx.get(), m.m, t.t), "fl_write_mesh");
+    t.write_to(out);
 }
 
 }  // namespace femlite_b200

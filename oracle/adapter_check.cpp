@@ -9,9 +9,12 @@
 #include <algorithm>
 #include <cstring>
 #include <numbers>
+#include <sstream>
 #include <vector>
 
 #include "femlite/assembly.hpp"
+#include "femlite/matrix_market.hpp"
+#include "femlite/mesh_io.hpp"
 #include "femlite/mesh.hpp"
 #include "femlite/solver.hpp"
 #include "femlite/sparse.hpp"
@@ -108,6 +111,14 @@ void run(const char* name, const femlite::Mesh& mesh) {
         for (index_t k = 0; k < a.m; k += 2) rows.push_back(k);
         for (index_t k = 1; k < a.n; k += 3) cols.push_back(k);
         expect(submatrix(a, rows, cols) == femlite_b200::submatrix(a, rows, cols), "submatrix", name);
+        // text writers (matrix_market.hpp:15-24, mesh_io.hpp:125-142): the same bytes
+        std::ostringstream r1, g1, r2, g2;
+        write_matrix_market(a, r1);
+        femlite_b200::write_matrix_market(a, g1);
+        expect(r1.str() == g1.str(), "write_matrix_market", name);
+        write_mesh(mesh, r2);
+        femlite_b200::write_mesh(mesh, g2);
+        expect(r2.str() == g2.str(), "write_mesh", name);
     }
 }
 

@@ -53,9 +53,9 @@ namespace fl {
 enum : int { G_NUM = 0, G_ZERO = 1, G_INF = 2, G_NAN = 3 };
 
 struct G17 {
-    uint64_t n;   // significant digits, trailing zeros stripped (nd digits)
-    int32_t x;    // decimal exponent of the first digit
-    int16_t nd;   // digits in n (1..17)
+    uint32_t h, l;  // the 17 significant digits: h = first 9, l = last 8
+    int32_t x;      // decimal exponent of the first digit
+    int16_t nd;     // significant digits left after stripping trailing zeros (1..17)
     int8_t kind;  // G_*
     int8_t neg;
 };
@@ -203,7 +203,7 @@ __device__ G17 g17(double v, bool force_exact) {
     g.neg = (int8_t)(bits >> 63);
     const int eb = (int)((bits >> 52) & 0x7ff);
     const uint64_t frac = bits & ((1ull << 52) - 1);
-    g.n = 0;
+    g.h = g.l = 0;
     g.x = 0;
     g.nd = 1;
     if (eb == 0x7ff) {
@@ -217,7 +217,8 @@ __device__ G17 g17(double v, bool force_exact) {
     g.kind = G_NUM;
     const uint64_t m = eb ? (frac | (1ull << 52)) : frac;
     const int e = eb ? eb - 1075 : -1074;
-    int x = (int)floor(log10(fabs(v)));
+    // floor(log10 |v|) or one less: floor((bit length - 1 + e) log10 2)
+    int x = ((63 - __clzll((long long)m) + e) * 1262611) >> 22;
     constexpr uint64_t E16 = 10000000000000000ull, E17 = 100000000000000000ull;
     uint64_t n = 0;
     // X is right when 10^16 <= |v| 10^(16-X) < 10^17 for the TRUE value (before
@@ -239,12 +240,20 @@ __device__ G17 g17(double v, bool force_exact) {
         }
         break;
     }
+    const uint32_t h = (uint32_t)(n / 100000000ull);
+    const uint32_t l = (uint32_t)(n - (uint64_t)h * 100000000ull);
     int nd = 17;
-    while (n % 10 == 0) {
-        n /= 10;
+    uint32_t t = l;
+    if (t == 0) {
+        nd = 9;
+        t = h;
+    }
+    while (t % 10 == 0) {
+        t /= 10;
         --nd;
     }
-    g.n = n;
+    g.h = h;
+    g.l = l;
     g.x = x;
     g.nd = (int16_t)nd;
     return g;
@@ -280,10 +289,16 @@ __device__ __forceinline__ int g17_emit(const G17& g, char* d) {
     }
     char dg[17];
     {
-        uint64_t n = g.n;
-        for (int i = g.nd - 1; i >= 0; --i) {
-            dg[i] = (char)('0' + n % 10);
-            n /= 10;
+        uint32_t a = g.h, b = g.l;
+#pragma unroll
+        for (int i = 16; i >= 9; --i) {
+            dg[i] = (char)('0' + b % 10);
+            b /= 10;
+        }
+#pragma unroll
+        for (int i = 8; i >= 0; --i) {
+            dg[i] = (char)('0' + a % 10);
+            a /= 10;
         }
     }
     const int x = g.x, nd = g.nd;
