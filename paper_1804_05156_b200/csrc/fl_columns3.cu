@@ -614,6 +614,23 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
     }
 }
 
+// element-first records into the result's erec buffers (p.srec / p.lrec)
+int launch_elem_records(fl_ctx* ctx, int dim, ColParams& p, fl_result* res) {
+    const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
+    FL_TRY(res->erec[0].ensure(sizeof(double) * 4 * (dim + 1) * ne));
+    if (dim == 3) FL_TRY(res->erec[1].ensure(sizeof(double) * 4 * ne));
+    p.srec = res->erec[0].as<double>();
+    p.lrec = dim == 3 ? res->erec[1].as<double>() : nullptr;
+    if (p.n_elems > 0) {
+        const int g = std::min(div_up(p.n_elems, kElemThreads), ctx->sm_count * 16);
+        if (dim == 3) k_elem_records<3><<<g, kElemThreads, 0, ctx->stream>>>(p);
+        else k_elem_records<2><<<g, kElemThreads, 0, ctx->stream>>>(p);
+        count_launch(ctx);
+        FL_CUDA(cudaGetLastError());
+    }
+    return FL_OK;
+}
+
 template <int D, int L, bool PRE, bool LIFT, int K>
 static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
     using C = V3<D, L, K>;
@@ -622,18 +639,7 @@ static int launch3(fl_ctx* ctx, ColParams& p, fl_result* res, bool finish) {
         FL_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
         ctx->kernel_timed = true;
     }
-    if constexpr (PRE) {
-        const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
-        FL_TRY(res->erec[0].ensure(sizeof(double) * 4 * (D + 1) * ne));
-        if (D == 3) FL_TRY(res->erec[1].ensure(sizeof(double) * 4 * ne));
-        p.srec = res->erec[0].as<double>();
-        p.lrec = D == 3 ? res->erec[1].as<double>() : nullptr;
-        if (p.n_elems > 0) {
-            const int g = std::min(div_up(p.n_elems, kElemThreads), ctx->sm_count * 16);
-            k_elem_records<D><<<g, kElemThreads, 0, ctx->stream>>>(p);
-            count_launch(ctx);
-        }
-    }
+    if constexpr (PRE) FL_TRY(launch_elem_records(ctx, D, p, res));
     int per_sm = 1;
     FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns3<D, L, PRE, LIFT, K>,
                                                           C::WARPS * 32, 0));

@@ -90,6 +90,8 @@ int launch_columns2(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res
 int launch_columns3(fl_ctx* ctx, int dim, ColParams& p, int kmax, fl_result* res, bool pre,
                     bool finish = true);
 int columns3_lanes(int dim, int kmax);
+int launch_elem_records(fl_ctx* ctx, int dim, ColParams& p, fl_result* res);
+
 int launch_neumann_add(fl_ctx* ctx, int dim, ColParams& p, fl_result* res);
 int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* res, bool pre);
 int prepare_staging(fl_ctx* ctx, ColParams& p, fl_result* res, int tc, int64_t cap);
