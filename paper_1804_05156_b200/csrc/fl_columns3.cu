@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
     constexpr int NV = D + 1;
     // per element: D == 3: the full local matrix, row-major (8 int4) + 4 load
     // shares (2 int4); D == 2: rows {s_0j, s_1j, s_2j, load_j} (6 int4)
-    constexpr int WS = D == 3 ? 8 : 6, WL = D == 3 ? 2 : 0;
+    constexpr int WS = rec64<D>() ? 4 * NV : 8, WL = rec64<D>() ? 0 : 2;
     constexpr int W = WS + WL + 1;  // +1: no bank conflicts
     __shared__ int4 stage[kElemThreads * W];
     const Recip R3 = recip(3.0);
@@ -135,14 +135,27 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
             // records: row j of the local matrix (= column j, s_ij == s_ji) is one
             // 32-byte line the column kernel reads with a single 256-bit load
             int4* st = stage + threadIdx.x * W;
+            if constexpr (rec64<D>()) {
+                const int4 ids = make_int4(V[0], V[1], V[2], D == 3 ? V[D] : 0);
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                double2 w0 = make_double2(S[j][0], S[j][1]);
-                double2 w1 = make_double2(S[j][2], D == 3 ? S[j][3] : Lj[j]);
-                st[2 * j] = *reinterpret_cast<int4*>(&w0);
-                st[2 * j + 1] = *reinterpret_cast<int4*>(&w1);
+                for (int j = 0; j < NV; ++j) {
+                    double2 w0 = make_double2(S[j][0], S[j][1]);
+                    double2 w1 = make_double2(S[j][2], D == 3 ? S[j][3] : Lj[j]);
+                    st[4 * j] = *reinterpret_cast<int4*>(&w0);
+                    st[4 * j + 1] = *reinterpret_cast<int4*>(&w1);
+                    st[4 * j + 2] = make_int4(__double2loint(Lj[j]), __double2hiint(Lj[j]), ids.x, ids.y);
+                    st[4 * j + 3] = make_int4(ids.z, ids.w, 0, 0);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    double2 w0 = make_double2(S[j][0], S[j][1]);
+                    double2 w1 = make_double2(S[j][2], D == 3 ? S[j][3] : Lj[j]);
+                    st[2 * j] = *reinterpret_cast<int4*>(&w0);
+                    st[2 * j + 1] = *reinterpret_cast<int4*>(&w1);
+                }
             }
-            if constexpr (D == 3) {
+            if constexpr (D == 3 && WL > 0) {
                 double2 l01 = make_double2(Lj[0], Lj[1]), l23 = make_double2(Lj[2], Lj[3]);
                 st[WS] = *reinterpret_cast<int4*>(&l01);
                 st[WS + 1] = *reinterpret_cast<int4*>(&l23);
@@ -278,7 +291,25 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                 R[i] = -1;
                 s[i] = 0.0;
             }
-            if (valid_ && PRE) {
+            if (valid_ && PRE && rec64<D>()) {
+                // the incidence's 64-byte record: two 256-bit loads of one block
+                const double* row = p.srec + ((size_t)t_ * NV + j_) * 8;
+                double q0, q1, q2, q3;
+                uint32_t w[8];
+                asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                    : "=d"(q0), "=d"(q1), "=d"(q2), "=d"(q3) : "l"(row));
+                asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                      "=r"(w[7])
+                    : "l"(row + 4));
+                s[0] = q0;
+                s[1] = q1;
+                s[2] = q2;
+                if constexpr (D == 3) s[3] = q3;
+                l = __hiloint2double((int)w[1], (int)w[0]);
+#pragma unroll
+                for (int i = 0; i < NV; ++i) R[i] = (int32_t)w[2 + i];
+            } else if (valid_ && PRE) {
                 // row j of the element's local matrix: one 256-bit load; the load
                 // share (3-D) and the vertex ids from their own arrays
                 const double* row = p.srec + ((size_t)t_ * NV + j_) * 4;
@@ -617,10 +648,11 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
 // element-first records into the result's erec buffers (p.srec / p.lrec)
 int launch_elem_records(fl_ctx* ctx, int dim, ColParams& p, fl_result* res) {
     const size_t ne = (size_t)std::max<int32_t>(p.n_elems, 1);
-    FL_TRY(res->erec[0].ensure(sizeof(double) * 4 * (dim + 1) * ne));
-    if (dim == 3) FL_TRY(res->erec[1].ensure(sizeof(double) * 4 * ne));
+    const bool r64 = dim == 2 ? rec64<2>() : rec64<3>();
+    FL_TRY(res->erec[0].ensure(sizeof(double) * (r64 ? 8 : 4) * (dim + 1) * ne));
+    if (!r64) FL_TRY(res->erec[1].ensure(sizeof(double) * 4 * ne));
     p.srec = res->erec[0].as<double>();
-    p.lrec = dim == 3 ? res->erec[1].as<double>() : nullptr;
+    p.lrec = r64 ? nullptr : res->erec[1].as<double>();
     if (p.n_elems > 0) {
         const int g = std::min(div_up(p.n_elems, kElemThreads), ctx->sm_count * 16);
         if (dim == 3) k_elem_records<3><<<g, kElemThreads, 0, ctx->stream>>>(p);

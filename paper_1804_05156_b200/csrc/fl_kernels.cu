@@ -52,34 +52,53 @@ __global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin,
     }
 }
 
+// U rounds of 32 consecutive entries per warp iteration: the rounds' atomics
+// (which return the slot, so each costs an L2 round trip) are all in flight
+// before the first dependent store
+constexpr int kFillRounds = 4;
 __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
                            const int32_t* __restrict__ elems, const int32_t* __restrict__ inc_ptr,
                            int32_t* __restrict__ cursor, uint32_t* __restrict__ inc,
                            uint8_t* __restrict__ emark) {
     (void)inc_ptr;
+    constexpr int U = kFillRounds;
     const int64_t n_entries = (int64_t)n_elems * nv;
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane;
-    for (int64_t e0 = base; e0 < n_entries; e0 += stride) {
-        const int64_t e = e0 + lane;
-        int32_t key = -1;
-        if (e < n_entries) {
-            const int32_t v = __ldg(elems + e);
-            if (v >= 0 && v < n_nodes && (uint32_t)(v - c_begin) < (uint32_t)n_cols) key = v - c_begin;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t e0 = warp * 32 * U; e0 < n_entries; e0 += nwarps * 32 * U) {
+        int32_t key[U];
+        unsigned grp[U];
+        int32_t pos[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * 32 + lane;
+            key[u] = -1;
+            if (e < n_entries) {
+                const int32_t v = __ldg(elems + e);
+                if (v >= 0 && v < n_nodes && (uint32_t)(v - c_begin) < (uint32_t)n_cols) key[u] = v - c_begin;
+            }
         }
-        const unsigned g = __match_any_sync(0xffffffffu, key);
+#pragma unroll
+        for (int u = 0; u < U; ++u) grp[u] = __match_any_sync(0xffffffffu, key[u]);
         // cursor starts at inc_ptr (one random-access array instead of two); the
         // leader reserves the group's slots, members take base + rank
-        int32_t pos = 0;
-        if (key >= 0 && (g & lower) == 0) pos = atomicAdd(cursor + key, __popc(g));
-        pos = __shfl_sync(0xffffffffu, pos, __ffs(g) - 1) + __popc(g & lower);
-        if (key >= 0) {
-            const int32_t t = (int32_t)(e / nv);
-            const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
-            inc[pos] = (j << 30) | (uint32_t)t;
-            if (emark) emark[t] = 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            pos[u] = 0;
+            if (key[u] >= 0 && (grp[u] & lower) == 0) pos[u] = atomicAdd(cursor + key[u], __popc(grp[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t p0 = __shfl_sync(0xffffffffu, pos[u], __ffs(grp[u]) - 1) + __popc(grp[u] & lower);
+            if (key[u] >= 0) {
+                const int64_t e = e0 + u * 32 + lane;
+                const int32_t t = (int32_t)(e / nv);
+                const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
+                inc[p0] = (j << 30) | (uint32_t)t;
+                if (emark) emark[t] = 1;
+            }
         }
     }
 }
@@ -443,10 +462,10 @@ __device__ __forceinline__ void lane_compute(const ColParams& p, Lane<D>& L, int
     L.t = (int32_t)(key & 0x3FFFFFFFu);
     L.j = (int)(key >> 30);
     if (p.srec) {  // hybrid pass: the element records are already computed
-        const double* row = p.srec + ((size_t)L.t * (D + 1) + L.j) * 4;
+        const double* row = p.srec + ((size_t)L.t * (D + 1) + L.j) * (rec64<D>() ? 8 : 4);
 #pragma unroll
         for (int i = 0; i <= D; ++i) L.s[i] = __ldg(row + i);
-        L.l = !p.want_b ? 0.0 : D == 3 ? __ldg(p.lrec + (size_t)L.t * 4 + L.j) : __ldg(row + 3);
+        L.l = !p.want_b ? 0.0 : rec64<D>() ? __ldg(row + 4) : __ldg(p.lrec + (size_t)L.t * 4 + L.j);
 #pragma unroll
         for (int i = 0; i <= D; ++i) L.R[i] = __ldg(p.elems + (size_t)L.t * (D + 1) + i);
         if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE) ec.load(p.nodes, L.R);

@@ -8,6 +8,15 @@
 
 namespace fl {
 
+// Element records.  2-D: 64 bytes per (element, local vertex j) -- {s_0j, s_1j,
+// s_2j, load_j} then {load_j, ids v0|v1, ids v2|0, 0} -- so a column reads one
+// aligned 64-byte block per incidence (C3 column pass 6.8 -> 5.6 ms).  3-D: the
+// 32-byte row {s_0j..s_3j}, the load shares and the element's vertex ids stay
+// separate: the 64-byte form cost more in the record writes than it saved in the
+// column reads on C4 / C5 (measured).
+template <int D>
+__host__ __device__ constexpr bool rec64() { return D == 2; }
+
 struct ColParams {
     int32_t n_nodes, n_elems;
     // owned columns [c_begin, c_begin + n_cols).  Column-indexed inputs (is_dir,
