@@ -82,7 +82,7 @@ __device__ __forceinline__ double node_field3(const FieldDesc& g, const double* 
 constexpr int kElemThreads = 128;
 
 template <int D>
-__global__ void __launch_bounds__(kElemThreads, 6) k_elem_records(ColParams p) {
+__global__ void __launch_bounds__(kElemThreads, D == 3 ? 8 : 6) k_elem_records(ColParams p) {
     constexpr int NV = D + 1;
     // per element: D == 3: the full local matrix, row-major (8 int4) + 4 load
     // shares (2 int4); D == 2: rows {s_0j, s_1j, s_2j, load_j} (6 int4)
