@@ -305,13 +305,10 @@ __global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ ele
     constexpr int NV = D + 1;
     const int64_t n_entries = (int64_t)n_elems * NV;
     uint32_t dir_faces = 0, neu_faces = 0, err = 0;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int8_t f = flags[e];
-        if (f == 0) continue;
+    auto visit = [&](int64_t e, int8_t f) {
         if (f == 3) err |= DERR_ROBIN;
         if (f < 0 || f > 3) err |= DERR_FLAG;
-        if (f != 1 && f != 2) continue;
+        if (f != 1 && f != 2) return;
         const int32_t t = (int32_t)(e / NV);
         const int lf = (int)(e - (int64_t)t * NV);
         int8_t* mark = (f == 1) ? is_dir : is_neu;
@@ -320,6 +317,24 @@ __global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ ele
 #pragma unroll
         for (int k = 0; k < NV; ++k)
             if (k != lf) mark[elems[(size_t)t * NV + k]] = 1;
+    };
+    // 16 flags per load: nearly all are 0 (interior faces)
+    const int64_t n_vec = n_entries >> 4;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < n_vec; i += stride) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(flags) + i);
+        if ((v.x | v.y | v.z | v.w) == 0) continue;
+        const int32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int8_t f = (int8_t)(w[b >> 2] >> (8 * (b & 3)));
+            if (f != 0) visit(i * 16 + b, f);
+        }
+    }
+    for (int64_t e = (n_vec << 4) + tid; e < n_entries; e += stride) {
+        const int8_t f = flags[e];
+        if (f != 0) visit(e, f);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
