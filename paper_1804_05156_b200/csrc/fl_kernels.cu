@@ -188,13 +188,23 @@ __global__ void __launch_bounds__(kPlanBlock)
 k_inc_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage,
              const int32_t* __restrict__ inc_ptr, int32_t* __restrict__ cursor,
              uint32_t* __restrict__ inc, uint8_t* __restrict__ emark) {
+    // four consecutive staged incidences per thread: their slot reservations are
+    // in flight together before the dependent stores
     const int64_t n_staged = *total;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_staged;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int2 s = __ldg(stage + q);
-        const int32_t pos = atomicAdd(cursor + s.x, 1);  // cursor starts at inc_ptr
-        inc[pos] = (uint32_t)s.y;
-        if (emark) emark[(uint32_t)s.y & 0x3FFFFFFFu] = 1;
+    for (int64_t q0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; q0 < n_staged;
+         q0 += (int64_t)gridDim.x * blockDim.x * 4) {
+        int2 sv[4];
+        int32_t pos[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sv[u] = q0 + u < n_staged ? __ldg(stage + q0 + u) : make_int2(-1, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pos[u] = sv[u].x >= 0 ? atomicAdd(cursor + sv[u].x, 1) : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (sv[u].x < 0) continue;
+            inc[pos[u]] = (uint32_t)sv[u].y;
+            if (emark) emark[(uint32_t)sv[u].y & 0x3FFFFFFFu] = 1;
+        }
     }
 }
 
@@ -961,6 +971,7 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
     // as many buckets of 2^shift nodes as the block histograms hold: a bucket's
     // slice of the incidence array (~3 MB at C5) stays in L2 while it is filled
     int shift = 0;
+    // (fewer buckets -- longer runs per bucket in the scatter -- measured slower on C3)
     while (nc > 0 && ((int64_t)(nc - 1) >> shift) + 1 > kMaxBuckets) ++shift;
     const int nb = nc > 0 ? ((nc - 1) >> shift) + 1 : 0;
     int32_t* bcnt = nullptr;
