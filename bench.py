@@ -126,8 +126,19 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # reference CPU path on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = None):
-    """Time femlite's own solve_poisson pre-solve path (oracle/_ref) on a sample."""
+def cpu_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = None,
+                  threads: int | None = None):
+    """Time femlite's own solve_poisson pre-solve path (oracle/_ref) on a sample,
+    on every host thread: the reference is single-threaded by construction, so T
+    threads each run the whole path on the sample concurrently and the value is
+    T x NT elements per wall-clock round (throughput with all host cores)."""
     from oracle import pyoracle as po
     from paper_1804_05156_b200 import configs
     if not po.have_ref():
@@ -138,20 +149,22 @@ def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = 
     coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
     f_kind = po.FIELD_SINSIN if cfg.f == "sinsin" else po.FIELD_CONST
     f_val = 0.0 if cfg.f == "sinsin" else float(cfg.f)
-    secs, nnz, nnz_ff = po.ref_time_system(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val,
-                                           coef, reps=1)
+    T = threads or cpu_threads()
+    secs = po.ref_time_system_mt(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val, coef, reps=1,
+                                 threads=T)
     one = float(secs[0])
     if reps is None:
         reps = max(1, min(5, int(seconds_budget / max(one, 1e-6))))
-    if reps > 1:
-        secs, nnz, nnz_ff = po.ref_time_system(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val,
-                                               coef, reps=reps)
+    secs = po.ref_time_system_mt(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val, coef, reps=reps,
+                                 threads=T)
+    _, nnz, _ = po.ref_time_system(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val, coef, reps=1)
     med = float(np.median(secs))
-    return {"value": m.num_elems() / med, "unit": UNIT, "cores": 1, "kind": "reference",
-            "seconds_per_step": med, "reps": int(len(secs)), "n_elems": m.num_elems(),
-            "sample": (f"{cfg.description} (n={n}, NT={m.num_elems()}, nnz={nnz}): femlite "
-                       "partition_boundary+assemble_blockwise+assemble_load+apply_neumann+"
-                       "apply_dirichlet+submatrix+b_f, 1 thread (the reference is single-threaded)")}
+    return {"value": T * m.num_elems() / med, "unit": UNIT, "cores": T, "kind": "reference",
+            "seconds_per_step": med, "reps": int(len(secs)), "n_elems": T * m.num_elems(),
+            "sample": (f"{cfg.description} (n={n}, NT={m.num_elems()}, nnz={nnz}) on each of {T} host "
+                       "threads concurrently: femlite partition_boundary+assemble_blockwise+"
+                       "assemble_load+apply_neumann+apply_dirichlet+submatrix+b_f (the reference is "
+                       "single-threaded; T independent runs = throughput on all cores)")}
 
 
 def run_reference_impl(args, rank: int, world: int):
@@ -161,13 +174,17 @@ def run_reference_impl(args, rank: int, world: int):
     if not po.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    per_step = []
-    base = None
-    for s in range(args.warmup + args.steps):
-        r = cpu_reference(args.config, reps=1)
-        if s >= args.warmup:
-            per_step.append(r["seconds_per_step"])
-            base = r
+    # one round = the sample assembled on every host thread at once; W + K rounds
+    base = cpu_reference(args.config, reps=1)
+    from paper_1804_05156_b200 import configs
+    cfg = configs.build(args.config, n=CPU_SAMPLE_N[args.config])
+    m = cfg.mesh
+    coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
+    f_kind = po.FIELD_SINSIN if cfg.f == "sinsin" else po.FIELD_CONST
+    f_val = 0.0 if cfg.f == "sinsin" else float(cfg.f)
+    secs = po.ref_time_system_mt(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val, coef,
+                                 reps=args.warmup + args.steps, threads=base["cores"])
+    per_step = list(secs[args.warmup:])
     ms = 1e3 * float(np.mean(per_step))
     value = base["n_elems"] / (ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -175,7 +192,7 @@ def run_reference_impl(args, rank: int, world: int):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config} sample", "sample": base["sample"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": "reference",
                              "sample": base["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -399,6 +399,20 @@ def ref_time_system(dim, nodes, elems, flags, f_kind, f_value=0.0, coef=None, re
     return secs, nnz.value, nnz_ff.value
 
 
+def ref_time_system_mt(dim, nodes, elems, flags, f_kind, f_value=0.0, coef=None, reps=1, threads=1):
+    """The reference pipeline on `threads` host threads concurrently (throughput);
+    per-round wall seconds (ref_shim.cpp ref_time_system_mt)."""
+    L = lib("ref")
+    nodes, elems, flags = _arr_f64(nodes), _arr_i32(elems), _arr_i8(flags)
+    coef = _arr_f64(coef) if coef is not None else None
+    secs = np.zeros(reps, dtype=np.float64)
+    _check(L.ref_time_system_mt(C.c_int(dim), C.c_int32(nodes.shape[0]), C.c_int32(elems.shape[0]),
+                                _p(nodes, _f64p), _p(elems, _i32p), _p(flags, _i8p), C.c_int(f_kind),
+                                C.c_double(f_value), _p(coef, _f64p), C.c_int(reps), C.c_int(threads),
+                                _p(secs, _f64p)), "ref")
+    return secs
+
+
 def ref_matvec(a: Csc, x):
     """The reference's matvec (sparse.hpp:129-141)."""
     L = lib("ref")

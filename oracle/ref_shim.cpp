@@ -30,7 +30,10 @@
 #include <cstring>
 #include <numbers>
 #include <sstream>
+#include <atomic>
+#include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "femlite/femlite.hpp"
@@ -348,6 +351,47 @@ int ref_time_system(int dim, int32_t n_nodes, int32_t n_elems, const double* nod
             nnz_ff_out[0] = a_ff.nnz();
             (void)part;
         }
+    });
+}
+
+// The same pipeline on `threads` host threads at once, each on its own copy of
+// the pipeline's outputs over the shared (read-only) mesh: the reference is
+// single-threaded by construction, so "all host threads" is throughput --
+// threads x NT elements per wall-clock step.  seconds_out[r] = wall time of
+// round r (all threads started together, timed until the last one finishes).
+int ref_time_system_mt(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                       const int32_t* elems, const int8_t* flags, int f_kind, double f_value,
+                       const double* coef, int reps, int threads, double* seconds_out) {
+    return guarded([&] {
+        const Mesh m = mesh_from(dim, n_nodes, n_elems, nodes, elems, flags);
+        const ScalarField f = make_field(f_kind, f_value, nullptr, nullptr);
+        const ScalarField zero = [](const Point&) { return 0.0; };
+        std::atomic<int> failed{0};
+        auto work = [&]() {
+            try {
+                const BoundaryPartition part = partition_boundary(m);
+                const CscMatrix a = coef ? blockwise_with_coefficient(m, coef) : assemble_blockwise(m);
+                std::vector<double> b = assemble_load(m, f);
+                b = apply_neumann(std::move(b), m, nullptr);
+                DirichletSystem sys = apply_dirichlet(a, b, m, zero);
+                const std::vector<index_t>& fr = sys.partition.free_nodes;
+                const CscMatrix a_ff = submatrix(a, fr, fr);
+                std::vector<double> b_f(fr.size());
+                for (std::size_t k = 0; k < fr.size(); ++k) b_f[k] = sys.b[std::size_t(fr[k])];
+                (void)part;
+                (void)a_ff;
+            } catch (...) {
+                failed = 1;
+            }
+        };
+        for (int r = 0; r < reps; ++r) {
+            std::vector<std::thread> pool;
+            const auto t0 = std::chrono::steady_clock::now();
+            for (int k = 0; k < threads; ++k) pool.emplace_back(work);
+            for (auto& t : pool) t.join();
+            seconds_out[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        if (failed) throw std::runtime_error("a worker thread failed");
     });
 }
 
