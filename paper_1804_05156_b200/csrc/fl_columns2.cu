@@ -691,42 +691,61 @@ __global__ void __launch_bounds__(THR) k_columns2(ColParams p) {
 // col_ptr[c+1] = tile_off + the in-tile inclusive count (same for A(free,free),
 // whose columns are the free columns in ascending order).
 __global__ void k_stage_copy(ColParams p, int tc) {
+    // a warp places kGroup consecutive tiles: their destinations are one
+    // contiguous run, so every store instruction writes 32 consecutive entries
+    constexpr int kGroup = 4;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int32_t* off_a = p.tile_off;
-    const int32_t* off_f = p.tile_off + p.n_tiles + 1;
-    const int32_t* tot_a = p.tile_tot;
-    const int32_t* tot_f = p.tile_tot + p.n_tiles + 1;
-    for (int64_t t = warp; t < p.n_tiles; t += nwarps) {
-        const int64_t sbase = t * p.tile_cap;
-        const int32_t oa = off_a[t], na = tot_a[t];
-        if ((int64_t)oa + na > p.cap_a) {
-            if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
-            continue;
-        }
-        for (int q = lane; q < na; q += 32) {
-            p.row_idx[oa + q] = p.st_a_row[sbase + q];
-            p.values[oa + q] = p.st_a_val[sbase + q];
-        }
-        const int32_t c0 = (int32_t)(t * tc);  // local column
-        for (int q = lane; q < tc && c0 + q < p.n_cols; q += 32)
-            p.col_ptr[c0 + q + 1] = oa + p.colcnt_a[c0 + q];
-        if (p.want_sys) {
-            const int32_t of = off_f[t], nf = tot_f[t];
-            for (int q = lane; q < nf; q += 32) {
-                p.ff_row_idx[of + q] = p.st_f_row[sbase + q];
-                p.ff_values[of + q] = p.st_f_val[sbase + q];
+    const int64_t ngroups = (p.n_tiles + kGroup - 1) / kGroup;
+    for (int64_t gidx = warp; gidx < ngroups; gidx += nwarps) {
+        const int64_t t0 = gidx * kGroup;
+        const int nt = (int)min((int64_t)kGroup, p.n_tiles - t0);
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {  // 0: A, 1: A(free, free)
+            if (f == 1 && !p.want_sys) break;
+            const int32_t* off = p.tile_off + (f ? p.n_tiles + 1 : 0);
+            const int32_t* tot = p.tile_tot + (f ? p.n_tiles + 1 : 0);
+            const int32_t* srow = f ? p.st_f_row : p.st_a_row;
+            const double* sval = f ? p.st_f_val : p.st_a_val;
+            int32_t* drow = f ? p.ff_row_idx : p.row_idx;
+            double* dval = f ? p.ff_values : p.values;
+            const int64_t cap = f ? p.cap_ff : p.cap_a;
+            const int32_t my_off = lane < nt ? off[t0 + lane] : 0;
+            const int32_t my_tot = lane < nt ? tot[t0 + lane] : 0;
+            const int32_t base = __shfl_sync(0xffffffffu, my_off, 0);
+            const int32_t end = __shfl_sync(0xffffffffu, my_off + my_tot, nt - 1);
+            if ((int64_t)end > cap) {
+                if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
+                continue;
             }
-            const int32_t fb = free_base(p);
-            for (int q = lane; q < tc && c0 + q < p.n_cols; q += 32) {
-                const int32_t fc = p.fidx[p.c_begin + c0 + q];
-                if (fc >= 0) p.ff_col_ptr[fc - fb + 1] = of + p.colcnt_f[c0 + q];
+            int32_t rel[kGroup];
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) rel[k] = __shfl_sync(0xffffffffu, my_off, k) - base;
+            for (int32_t q = lane; q < end - base; q += 32) {
+                int k = 0;
+#pragma unroll
+                for (int kk = 1; kk < kGroup; ++kk)
+                    if (kk < nt && q >= rel[kk]) k = kk;
+                const int64_t src = (t0 + k) * p.tile_cap + (q - rel[k]);
+                drow[base + q] = srow[src];
+                dval[base + q] = sval[src];
+            }
+        }
+        // col_ptr (and A(free,free) col_ptr): in-tile inclusive counts + tile offsets
+        const int32_t fb = free_base(p);
+        for (int q = lane; q < nt * tc; q += 32) {
+            const int k = q / tc;
+            const int32_t c = (int32_t)((t0 + k) * tc + (q - k * tc));
+            if (c >= p.n_cols) continue;
+            p.col_ptr[c + 1] = p.tile_off[t0 + k] + p.colcnt_a[c];
+            if (p.want_sys) {
+                const int32_t fc = p.fidx[p.c_begin + c];
+                if (fc >= 0) p.ff_col_ptr[fc - fb + 1] = p.tile_off[p.n_tiles + 1 + t0 + k] + p.colcnt_f[c];
             }
         }
     }
 }
-
 
 template <int D, int TCX, int THR, int KMAX, bool LIFT>
 static int launch_variant(fl_ctx* ctx, ColParams& p, fl_result* res) {
@@ -790,7 +809,7 @@ int finish_staging(fl_ctx* ctx, ColParams& p, int tc) {
             p.tile_off + p.n_tiles + 1, ctx->scan_ws.p, s));
         count_launch(ctx);
     }
-    const int64_t warps = std::min<int64_t>(p.n_tiles, (int64_t)ctx->sm_count * 64);
+    const int64_t warps = std::min<int64_t>((p.n_tiles + 3) / 4, (int64_t)ctx->sm_count * 64);
     k_stage_copy<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(p, tc);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
