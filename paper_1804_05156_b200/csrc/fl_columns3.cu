@@ -221,6 +221,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
             const int32_t lc = lc0 + q;  // owned column
             const bool act = q < ncol_t;
             const int32_t c = p.c_begin + lc;  // global node
+            // the column's partition data, loaded early (used after the folds)
+            const int32_t fc_c = (act && p.want_sys) ? __ldg(p.fidx + c) : -1;
+            const bool dir_c = act && p.want_sys && __ldg(p.is_dir + c);
             int32_t m = mn;
             uint32_t key[K];
 #pragma unroll
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                     }
                     __syncwarp();
                 }
-                const bool col_free = act && p.want_sys && __ldg(p.fidx + c) >= 0;
+                const bool col_free = fc_c >= 0;
                 int na = 0, nf = 0;
                 // compaction in chunks of L entries; pass 1: counts per group (one
                 // group per warp: the column starts at the warp's running count)
@@ -628,11 +631,11 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
             if (act && g == 0) {
                 if (p.want_b) p.b[lc] = b;
                 if (p.want_sys) {
-                    const double u0 = p.is_dir[c] ? node_field3(p.g_dir, p.nodes, D, c) : 0.0;
+                    const double u0 = dir_c ? node_field3(p.g_dir, p.nodes, D, c) : 0.0;
                     const double bmod = LIFT ? b - ylift : b - 0.0;  // system.hpp:197-198
                     p.u0[lc] = u0;
                     p.b_mod[lc] = bmod;
-                    const int32_t fc = p.fidx[c];
+                    const int32_t fc = fc_c;
                     if (fc >= 0) p.b_f[fc - free_base(p)] = bmod;
                 }
             }
