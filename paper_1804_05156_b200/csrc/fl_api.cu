@@ -591,6 +591,13 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             p.phase_cycles = ctx->phases.as<unsigned long long>();
             FL_CUDA(cudaMemsetAsync(p.phase_cycles, 0, sizeof(unsigned long long) * 8, s));
         }
+        // a cached plan used again: sort its segments once, the register kernel
+        // then skips its key sort on this and every later assembly of the mesh
+        const char* ks = std::getenv("FL_KEYSORT");
+        if (kk == '0' && !ctx->plan_timed && !(ks && ks[0] == '0')) {
+            if (!mesh->inc_sorted) FL_TRY(launch_inc_sort(ctx, mesh));
+            p.keys_sorted = true;
+        }
         x->last = p;
         x->last_mesh = mesh;
         x->last_valid = true;

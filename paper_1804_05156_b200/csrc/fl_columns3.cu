@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                 for (int kk = 0; kk < K; ++kk) key[kk] = 0xFFFFFFFFu;
             }
             // ---- 1. keys, sorted ascending inside the group: incidence e = kk*L + g
-            //      (bitonic over L*K; distances >= L pair registers of one lane)
+            //      (bitonic over L*K; distances >= L pair registers of one lane);
+            //      a cached plan's segments were sorted once (k_inc_sort)
+            if (!p.keys_sorted)
 #pragma unroll
             for (int k = 2; k <= LK; k <<= 1) {
 #pragma unroll

@@ -941,6 +941,7 @@ __global__ void k_selftest_div(int64_t n, const double* __restrict__ a, const do
 // ===========================================================================
 int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
     const cudaStream_t s = ctx->stream;
+    mesh->inc_sorted = false;
     const int nv = mesh->dim + 1;
     const int64_t n_entries = (int64_t)mesh->n_elems * nv;
     const int32_t N = mesh->n_nodes;
@@ -1038,6 +1039,7 @@ int launch_inc_sort(fl_ctx* ctx, fl_mesh* mesh) {
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
+    mesh->inc_sorted = true;
     return FL_OK;
 }
 

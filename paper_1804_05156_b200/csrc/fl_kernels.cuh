@@ -79,6 +79,7 @@ struct ColParams {
     int32_t* ov_off;
     unsigned long long* ov_alloc;  // [2] running A / A(free,free) overflow-staging tops
     const double* nadd;  // Neumann shares per owned column (k_neumann_add), nullptr = none
+    bool keys_sorted;    // the plan's segments are already in (j, t) order: no in-kernel sort
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
