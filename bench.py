@@ -399,6 +399,12 @@ def run_ours(args, rank: int, world: int):
         }
         if args.traffic:
             line["roofline"]["traffic"] = float(args.traffic)
+        if line["roofline"]["traffic"]:
+            # the DRAM bytes the kernels actually move (ncu) over the same live time:
+            # how close the phase runs to the HBM roofline for its access pattern
+            tg = line["roofline"]["traffic"] / (col_ms * 1e-3) / 1e9
+            line["roofline"]["traffic_gbs"] = tg
+            line["roofline"]["traffic_frac"] = tg / peak
         print(json.dumps(line))
     return line
 
