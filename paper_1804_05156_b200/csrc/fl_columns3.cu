@@ -595,14 +595,20 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                 int na = 0, nf = 0;
                 // compaction in chunks of L entries; pass 1: counts per group (one
                 // group per warp: the column starts at the warp's running count)
+                constexpr int NCH = (C::MAXS + L - 1) / L;
+                int32_t frc[NCH];  // free ranks of the chunk rows (pass 1 -> pass 2)
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) frc[ch] = -1;
                 if (L < 32)
-                for (int base = 0; base < C::MAXS; base += L) {
-                    const int q = base + g;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const int q = ch * L + g;
                     const bool in = q < nslot;
                     const double v = in ? sm.sval[q] : 0.0;
                     const int32_t r = in ? sm.srow[q] : 0;
                     const bool keep = in && v != 0.0;  // sparse.hpp:105
-                    const bool keepf = keep && col_free && __ldg(p.fidx + r) >= 0;
+                    frc[ch] = (keep && col_free) ? __ldg(p.fidx + r) : -1;
+                    const bool keepf = frc[ch] >= 0;
                     na += __popc(__ballot_sync(FULL, keep) & gmask);
                     nf += __popc(__ballot_sync(FULL, keepf) & gmask);
                 }
@@ -624,13 +630,14 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                     if (p.want_sys) p.colcnt_f[lc] = wf + nf;
                 }
                 // pass 2: write
-                for (int base = 0; base < C::MAXS; base += L) {
-                    const int q = base + g;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const int q = ch * L + g;
                     const bool in = q < nslot;
                     const double v = in ? sm.sval[q] : 0.0;
                     const int32_t r = in ? sm.srow[q] : 0;
                     const bool keep = in && v != 0.0;
-                    const int32_t fr = (keep && col_free) ? __ldg(p.fidx + r) : -1;
+                    const int32_t fr = L < 32 ? frc[ch] : ((keep && col_free) ? __ldg(p.fidx + r) : -1);
                     const bool keepf = fr >= 0;
                     const unsigned ba = __ballot_sync(FULL, keep) & gmask;
                     const unsigned bf = __ballot_sync(FULL, keepf) & gmask;
