@@ -525,9 +525,14 @@ __global__ void __launch_bounds__(V3<D, L>::WARPS * 32, PRE ? (K == 1 ? 10 : (L 
                                             acc = acc + sm.itm[i][kk * L + __ffs(mm) - 1];
                             } else {  // the passes' L-bit masks concatenated: bit b = itm[b / L][b % L]
                                 const double* flat = &sm.itm[0][0];
-                                const uint64_t w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) |
-                                                    ((uint64_t)mk4.z << (2 * L));
-                                for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
+                                if constexpr (3 * L <= 32) {  // L = 8: one 32-bit word
+                                    const uint32_t w0 = mk4.x | (mk4.y << L) | (mk4.z << (2 * L));
+                                    for (uint32_t w = w0; w; w &= w - 1) acc = acc + flat[__ffs(w) - 1];
+                                } else {
+                                    const uint64_t w0 = (uint64_t)mk4.x | ((uint64_t)mk4.y << L) |
+                                                        ((uint64_t)mk4.z << (2 * L));
+                                    for (uint64_t w = w0; w; w &= w - 1) acc = acc + flat[__ffsll(w) - 1];
+                                }
                             }
                             if constexpr (LIFT) {
                                 // A(c, r) folds the same items in (i_c*(d+1)+j_r, t) order: the
