@@ -28,16 +28,19 @@ namespace fl {
 // Consecutive entries of element-ordered meshes repeat vertices (the tets of a
 // Kuhn cube share 8 vertices over 24 entries): lanes holding the same node are
 // grouped with match_any and the group leader issues one atomic for all of them.
-__global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols,
+// Block-contiguous: block b counts entries [b*256*it, (b+1)*256*it), blocks
+// issued in element order, so the live counters stay in L2.  B200, it = 16 vs
+// a grid-stride loop: C5 plan 5.30 -> 5.16 ms, C4 0.48 -> 0.46 ms (it = 1,
+// one entry per thread: C5 +0.8 ms).
+constexpr int kCountIters = 16;
+__global__ void k_inc_count(int64_t n_entries, int32_t n_nodes, int32_t c_begin, int32_t n_cols, int it,
                             const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
                             uint32_t* __restrict__ err) {
     const unsigned lower = (1u << (threadIdx.x & 31)) - 1;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t start = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    // warp-uniform trip count: every lane reaches the match_any
-    const int64_t base = start - (threadIdx.x & 31);
-    for (int64_t e0 = base; e0 < n_entries; e0 += stride) {
-        const int64_t e = e0 + (threadIdx.x & 31);
+    const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * it;
+    for (int k = 0; k < it; ++k) {
+        const int64_t e = b0 + (int64_t)k * blockDim.x + threadIdx.x;
+        if (e - (threadIdx.x & 31) >= n_entries) break;  // warp-uniform
         int32_t key = -1;
         if (e < n_entries) {
             const int32_t v = __ldg(elems + e);
@@ -984,7 +987,11 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
                                                   mesh->elems.as<int32_t>(), cnt, bcnt, d_err);
         count_launch(ctx);
     } else if (n_entries > 0) {
-        k_inc_count<<<grid, 256, 0, s>>>(n_entries, N, c0, nc, mesh->elems.as<int32_t>(), cnt, d_err);
+        // up to kCountIters per block, fewer on small meshes so the grid still fills the SMs
+        const int it = (int)std::max<int64_t>(
+            1, std::min<int64_t>(kCountIters, n_entries / (256 * (int64_t)ctx->sm_count * 8)));
+        k_inc_count<<<(int)std::max<int64_t>(div_up(n_entries, 256 * (int64_t)it), 1), 256, 0, s>>>(
+            n_entries, N, c0, nc, it, mesh->elems.as<int32_t>(), cnt, d_err);
         count_launch(ctx);
     }
     const int32_t* cnt_c = cnt;
@@ -1022,8 +1029,7 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         // the live set of destination segments is one resident wave's worth and
         // stays in L2 until its sectors are complete (a grid-stride loop lets
         // warps drift apart and the partial sectors go back to DRAM).  B200:
-        // C5 plan 7.36 -> 5.31 ms, C4 0.53 -> 0.48 ms; the same launch for
-        // k_inc_count is slower (C5 +0.8 ms), so that one stays grid-stride.
+        // C5 plan 7.36 -> 5.31 ms, C4 0.53 -> 0.48 ms.
         // (4 rounds per warp measured best with this launch: C5 plan 5.96 / 5.55 /
         // 5.33 / 5.88 ms at 1 / 2 / 4 / 8)
         const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * kFillRounds), 1),
