@@ -722,14 +722,33 @@ __global__ void k_stage_copy(ColParams p, int tc) {
             int32_t rel[kGroup];
 #pragma unroll
             for (int k = 0; k < kGroup; ++k) rel[k] = __shfl_sync(0xffffffffu, my_off, k) - base;
-            for (int32_t q = lane; q < end - base; q += 32) {
-                int k = 0;
+            // four strides per round: all loads issued before the stores
+            constexpr int R = 4;
+            const int32_t n = end - base;
+            for (int32_t q0 = 0; q0 < n; q0 += 32 * R) {
+                int32_t rw[R];
+                double vv[R];
 #pragma unroll
-                for (int kk = 1; kk < kGroup; ++kk)
-                    if (kk < nt && q >= rel[kk]) k = kk;
-                const int64_t src = (t0 + k) * p.tile_cap + (q - rel[k]);
-                drow[base + q] = srow[src];
-                dval[base + q] = sval[src];
+                for (int r = 0; r < R; ++r) {
+                    const int32_t q = q0 + r * 32 + lane;
+                    if (q < n) {
+                        int k = 0;
+#pragma unroll
+                        for (int kk = 1; kk < kGroup; ++kk)
+                            if (kk < nt && q >= rel[kk]) k = kk;
+                        const int64_t src = (t0 + k) * p.tile_cap + (q - rel[k]);
+                        rw[r] = __ldcs(srow + src);
+                        vv[r] = __ldcs(sval + src);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t q = q0 + r * 32 + lane;
+                    if (q < n) {
+                        drow[base + q] = rw[r];
+                        dval[base + q] = vv[r];
+                    }
+                }
             }
         }
         // col_ptr (and A(free,free) col_ptr): in-tile inclusive counts + tile offsets
