@@ -1014,7 +1014,10 @@ int launch_plan_kernels(fl_ctx* ctx, fl_mesh* mesh, uint32_t* d_err) {
         FL_TRY(mesh->bstage.ensure(sizeof(int2) * (size_t)n_entries));
         int2* stage = mesh->bstage.as<int2>();
         const int64_t chunks = (n_entries + kPlanBlock * kPlanItems - 1) / (kPlanBlock * kPlanItems);
-        const int g2 = (int)std::min<int64_t>(chunks, (int64_t)ctx->sm_count * 8);
+        // one chunk per block, blocks issued in element order: consecutive chunks
+        // append to each bucket's run back to back (C3 plan 3.83 -> 3.70 ms vs a
+        // grid-stride loop over sm_count * 8 blocks)
+        const int g2 = (int)std::min<int64_t>(chunks, INT_MAX);
         k_bucket_scatter<<<g2, kPlanBlock, 0, s>>>(n_entries, nv, N, c0, nc, shift,
                                                    mesh->elems.as<int32_t>(), boff, bcur, stage);
         count_launch(ctx);
