@@ -144,9 +144,9 @@ def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = 
     if not po.have_ref():
         return None
     n = CPU_SAMPLE_N[config]
-    cfg = configs.build(config, n=n)
+    cfg = configs.build(config, n=n)  # numpy-only generators: no libfemlite_b200.so here
     m = cfg.mesh
-    coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
+    coef = po.coefficient_c5(m.dim, m.nodes, m.elems) if cfg.coef else None
     f_kind = po.FIELD_SINSIN if cfg.f == "sinsin" else po.FIELD_CONST
     f_val = 0.0 if cfg.f == "sinsin" else float(cfg.f)
     T = threads or cpu_threads()
@@ -167,6 +167,13 @@ def cpu_reference(config: str, seconds_budget: float = 25.0, reps: int | None = 
                        "single-threaded; T independent runs = throughput on all cores)")}
 
 
+def workload_name(config: str) -> str:
+    from paper_1804_05156_b200.configs import FULL_N
+    desc = {"C1": "unit_square:{n}", "C2": "lshape:{n} jittered", "C3": "unit_square:{n} permuted",
+            "C4": "unit_cube:{n}", "C5": "unit_cube:{n} permuted+coef"}[config]
+    return f"{config}: " + desc.format(n=FULL_N[config])
+
+
 def run_reference_impl(args, rank: int, world: int):
     if rank != 0:
         return
@@ -179,7 +186,7 @@ def run_reference_impl(args, rank: int, world: int):
     from paper_1804_05156_b200 import configs
     cfg = configs.build(args.config, n=CPU_SAMPLE_N[args.config])
     m = cfg.mesh
-    coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
+    coef = po.coefficient_c5(m.dim, m.nodes, m.elems) if cfg.coef else None
     f_kind = po.FIELD_SINSIN if cfg.f == "sinsin" else po.FIELD_CONST
     f_val = 0.0 if cfg.f == "sinsin" else float(cfg.f)
     secs = po.ref_time_system_mt(m.dim, m.nodes, m.elems, m.bd_flags, f_kind, f_val, coef,
@@ -191,7 +198,10 @@ def run_reference_impl(args, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.config} sample", "sample": base["sample"]},
+            # the same workload as our arm's line; each step times a bounded sample of
+            # it (the rate in elements/s is per element: see cpu_baseline.sample and
+            # profiles/ for the full-size single-thread check)
+            "config": {"workload": workload_name(args.config), "sample": base["sample"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": "reference",
                              "sample": base["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -338,14 +348,15 @@ def run_ours(args, rank: int, world: int):
     b_sl = configs.algorithmic_bytes(d, N, NT, nnz)
     b_sys = configs.system_bytes(d, N, NT, nnz, n_free, nnz_ff)
     f_bytes = 8 * NT * (d + 1) if ff.kind == _lib.FIELD_SAMPLES else 0
-    # numeric phase (element records + column kernel + placement), this rank:
-    # compulsory bytes = mesh + f samples read once, every column output written once
+    # the column kernel's own compulsory bytes (this rank): label-plan keys and
+    # relabelled elements read once, label-ordered nodes read once, staged entries
+    # and per-label vectors written once
     frac_el = 1.0 if world == 1 else min(1.0, ncol_l / max(N, 1) * 1.0)
-    col_bytes = (int(frac_el * (4 * (d + 1) * NT + 8 * d * N + f_bytes)) + ncol_l + 4 * ncol_l
-                 + 4 * (ncol_l + 1) + 12 * nnz_l + 8 * ncol_l + 16 * ncol_l
-                 + 4 * (nfree_l + 1) + 12 * nnz_ff_l + 8 * nfree_l)
+    kern_bytes = (int(frac_el * (8 * (d + 1) * NT + f_bytes)) + 32 * ncol_l
+                  + 12 * nnz_l + 12 * nnz_ff_l + 32 * ncol_l + 8 * ncol_l)
     peak, peak_kind = peaks()
-    achieved = col_bytes / (col_ms * 1e-3) / 1e9
+    # achieved = B_SL / t, t = the measured assembly (the whole step)
+    achieved = b_sl / (ms * 1e-3) / 1e9
     traffic = load_traffic(args.config) if world == 1 else None
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----
@@ -369,7 +380,7 @@ def run_ours(args, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator meshes, SURVEY.md §8(d) recipes)",
-            "config": {"workload": f"{args.config}: {cfg.description}", "n_nodes": N,
+            "config": {"workload": workload_name(args.config), "n_nodes": N,
                        "n_elems": NT, "nnz": nnz, "nnz_ff": nnz_ff, "n_free": n_free,
                        "step": "plan+partition+stiffness+load+dirichlet+A_ff+b_f",
                        "l2": ("flushed between steps (256 MB write)" if flush is not None
@@ -379,17 +390,26 @@ def run_ours(args, rank: int, world: int):
                        "f": str(cfg.f) if not isinstance(cfg.f, np.ndarray) else "host samples",
                        "coef": str(cfg.coef)},
             "hbm_gbs_step": b_sys / (ms * 1e-3) / 1e9,
-            "bytes": {"B_SL": b_sl, "B_sys": b_sys, "f_samples": f_bytes, "numeric_phase": col_bytes},
+            "bytes": {"B_SL": b_sl, "B_sys": b_sys, "f_samples": f_bytes, "column_kernel": kern_bytes},
             "phases_ms": {"plan": plan_ms, "partition": mark_ms, "numeric": col_ms,
                           "element_records": rec_ms, "column_kernel": kern_ms, "placement": place_ms},
             "roofline": {"bound": "hbm",
-                         "kernel": "numeric phase (k_elem_records + k_columns3 + placement), rank 0",
+                         "kernel": "the whole step (fl_assemble), SURVEY.md §8(d): achieved = B_SL / ms_per_step",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": traffic["dram_bytes"] if traffic else None,
-                         "traffic_source": traffic["source"] if traffic else None},
+                         "frac": achieved / peak, "algorithmic_bytes": b_sl,
+                         "traffic": traffic["step_dram_bytes"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "b_sys_frac": b_sys / (ms * 1e-3) / 1e9 / peak,
+                         "dominant_kernel": {
+                             "name": "k_columns4 (label-space column kernel)",
+                             "ms": kern_ms, "share_of_step": kern_ms / ms if ms > 0 else None,
+                             "compulsory_bytes": kern_bytes,
+                             "achieved": kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None,
+                             "frac": kern_bytes / (kern_ms * 1e-3) / 1e9 / peak if kern_ms > 0 else None,
+                             "traffic": traffic["kernel_dram_bytes"] if traffic else None}},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_single": e2e["single_call"] if e2e else None,
             "cached_plan": ({"value": NT / (float(np.mean([a.elapsed_time(b) for a, b in cached])) * 1e-3),
                              "unit": UNIT, "ms_per_step": float(np.mean([a.elapsed_time(b) for a, b in cached])),
                              "step": "partition+stiffness+load+dirichlet+A_ff+b_f on the cached plan"}
@@ -400,9 +420,8 @@ def run_ours(args, rank: int, world: int):
         if args.traffic:
             line["roofline"]["traffic"] = float(args.traffic)
         if line["roofline"]["traffic"]:
-            # the DRAM bytes the kernels actually move (ncu) over the same live time:
-            # how close the phase runs to the HBM roofline for its access pattern
-            tg = line["roofline"]["traffic"] / (col_ms * 1e-3) / 1e9
+            # the DRAM bytes the step's kernels actually move (ncu) over the step time
+            tg = line["roofline"]["traffic"] / (ms * 1e-3) / 1e9
             line["roofline"]["traffic_gbs"] = tg
             line["roofline"]["traffic_frac"] = tg / peak
         print(json.dumps(line))
@@ -484,6 +503,15 @@ def run_e2e(args, cfg, torch, fl, _lib, L, C, dev, cols=None):
     for k in range(max(K - depth + 1, 0), K):
         drain(slots[k % depth])
     sec = (time.perf_counter() - t0) / K
+    # single-call latency: one drop-in call at a time (upload -> assemble -> every
+    # output downloaded), nothing overlapped -- what one solve_poisson caller sees
+    singles = []
+    for _ in range(3):
+        t1 = time.perf_counter()
+        issue(slots[0])
+        drain(slots[0])
+        singles.append(time.perf_counter() - t1)
+    single = float(np.median(singles))
     h2d = h_nodes.numel() * 8 + h_elems.numel() * 4 + h_flags.numel() + (f_arr.nbytes if f_arr is not None else 0)
     d2h = sum(buf.numel() * buf.element_size() for _, buf in slots[0]["outs"])
     for sl in slots:
@@ -491,6 +519,9 @@ def run_e2e(args, cfg, torch, fl, _lib, L, C, dev, cols=None):
         del sl["res"]
     return {"value": NT / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": K,
+            "single_call": {"value": NT / single, "unit": UNIT, "ms": single * 1e3, "calls": len(singles),
+                            "timing": "median wall clock of one un-pipelined C-ABI call: H2D of the "
+                                      "mesh arrays from pinned memory, fl_assemble, every output D2H"},
             "timing": (f"wall clock over {K} steps, {depth}-deep pipeline of fl_ctx "
                        "(upload | assemble | download overlap across consecutive steps), "
                        "host arrays in pinned memory")}

@@ -12,6 +12,9 @@
 //                                                    partition, A, b, Neumann, Dirichlet lift,
 //                                                    A(free, free), b_f -- one fused pass)
 //   femlite_b200::submatrix(a, rows, cols)           sparse.hpp:159    submatrix
+//   femlite_b200::apply_dirichlet(a, b, mesh, g)     system.hpp:182    apply_dirichlet (any A, b)
+//   femlite_b200::from_triplets(t)                   sparse.hpp:61     from_triplets
+//   femlite_b200::accumulate(idx, vals, size)        sparse.hpp:186    accumulate
 //   femlite_b200::matvec / cg_solve / solve_poisson  sparse.hpp:129, solver.hpp:63, :223
 //   femlite_b200::write_matrix_market(a, out)        matrix_market.hpp:15 write_matrix_market
 //   femlite_b200::write_mesh(mesh, out)              mesh_io.hpp:125      write_mesh
@@ -148,14 +151,26 @@ inline fl_field samples(const std::vector<double>& v) {
     return fl_field{FL_FIELD_SAMPLES, FL_MEM_HOST, 0.0, v.data(), static_cast<int64_t>(v.size())};
 }
 
+/// boundary_faces(mesh, 1 | 2) (mesh.hpp:222-246) as the GPU produced them
+inline femlite::FaceList face_list_of(const femlite::Mesh& mesh, const ResultHandle& r, bool dirichlet) {
+    const fl_sizes z = r.sizes();
+    const int64_t n = dirichlet ? z.n_dir_faces : z.n_neu_faces;
+    femlite::FaceList f;
+    f.dim = mesh.dim();
+    f.faces = r.array<femlite::index_t>(dirichlet ? FL_DIR_FACES : FL_NEU_FACES, n * mesh.dim());
+    f.parent_elem = r.array<femlite::index_t>(dirichlet ? FL_DIR_FACE_ELEM : FL_NEU_FACE_ELEM, n);
+    const std::vector<int32_t> lf = r.array<int32_t>(dirichlet ? FL_DIR_FACE_LOCAL : FL_NEU_FACE_LOCAL, n);
+    f.local_face.assign(lf.begin(), lf.end());
+    return f;
+}
+
 inline femlite::BoundaryPartition partition_of(const femlite::Mesh& mesh, const ResultHandle& r) {
     const fl_sizes z = r.sizes();
     femlite::BoundaryPartition p;
     p.dirichlet_nodes = r.array<femlite::index_t>(FL_DIR_NODES, z.n_dir);
     p.free_nodes = r.array<femlite::index_t>(FL_FREE_NODES, z.n_free);
-    // the face lists are index bookkeeping of the reference's own mesh layer
-    p.dirichlet_faces = femlite::boundary_faces(mesh, 1);
-    p.neumann_faces = femlite::boundary_faces(mesh, 2);
+    p.dirichlet_faces = face_list_of(mesh, r, true);
+    p.neumann_faces = face_list_of(mesh, r, false);
     return p;
 }
 
@@ -223,8 +238,7 @@ inline std::vector<double> apply_neumann(std::vector<double> b, const femlite::M
     detail::ResultHandle r(ctx);
     const std::vector<double> gs = detail::sample(mesh, g, 3);
     const fl_field gn = detail::samples(gs), n = detail::none();
-    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &gn, FL_OUT_LOAD | FL_OUT_PARTITION, r.r),
-          "fl_assemble");
+    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &gn, FL_OUT_LOAD, r.r), "fl_assemble");
     const std::vector<double> add = r.array<double>(FL_B, r.sizes().n);
     for (std::size_t k = 0; k < b.size(); ++k) b[k] += add[k];
     return b;
@@ -299,20 +313,29 @@ inline femlite::CgResult cg_solve(const femlite::CscMatrix& a, std::span<const d
     return r;
 }
 
-/// solver.hpp:223-247 for meshes with Dirichlet faces: assembly, CG and the
-/// nodal scatter device-resident; throws max_iter_exceeded like solve_reduced
+/// solver.hpp:223-276 device-resident: with Dirichlet faces the free-node
+/// system (lift, A(free, free), b_f) and CG; without them the pure-Neumann path
+/// (compatibility, pinned node opts.pin_node, zero-average shift).  Throws
+/// max_iter_exceeded like solve_reduced.  SolveMethod::dense_direct is the
+/// reference's small-system CPU check (a dense factorisation guarded by
+/// kDenseGuardLimit): rejected here with invalid_parameter.
 inline femlite::Solution solve_poisson(const femlite::Mesh& mesh, const femlite::PoissonProblem& pb,
                                        const femlite::SolveOptions& opts = {},
                                        Context& ctx = Context::default_context()) {
+    if (opts.method == femlite::SolveMethod::dense_direct)
+        throw femlite::Error(femlite::ErrorCode::invalid_parameter,
+                             "dense_direct is the reference's CPU check; the B200 path solves with CG");
     detail::MeshHandle m(ctx, mesh);
     detail::ResultHandle r(ctx);
     std::vector<double> fs, gd, gn;
     fl_field ff = detail::none(), fd = detail::none(), fn = detail::none();
     const fl_field n = detail::none();
     if (pb.f) ff = detail::samples(fs = detail::sample(mesh, pb.f, 0));
-    if (pb.g_dirichlet) fd = detail::samples(gd = detail::sample_nodes(mesh, pb.g_dirichlet));
     if (pb.g_neumann) fn = detail::samples(gn = detail::sample(mesh, pb.g_neumann, 3));
-    check(fl_assemble(ctx.get(), m.m, &ff, &n, &fd, &fn, FL_OUT_SYSTEM, r.r), "fl_assemble");
+    // partition_boundary first (solver.hpp:226): Robin flags, Dirichlet or not
+    detail::ResultHandle part(ctx);
+    check(fl_assemble(ctx.get(), m.m, &n, &n, &n, &n, FL_OUT_PARTITION, part.r), "fl_assemble");
+    const bool dirichlet = part.sizes().n_dir_faces > 0;
     fl_cg_options o{opts.rel_tol, opts.max_iter,
                     opts.preconditioner == femlite::Preconditioner::none     ? 0
                     : opts.preconditioner == femlite::Preconditioner::jacobi ? 1
@@ -321,11 +344,70 @@ inline femlite::Solution solve_poisson(const femlite::Mesh& mesh, const femlite:
     femlite::Solution sol;
     sol.u.resize(static_cast<std::size_t>(mesh.num_nodes()));
     int64_t it = 0;
-    check(fl_solve_system(ctx.get(), r.r, &o, sol.u.data(), FL_MEM_HOST, &it, &sol.final_relres),
-          "fl_solve_system");
+    if (dirichlet) {
+        if (pb.g_dirichlet) fd = detail::samples(gd = detail::sample_nodes(mesh, pb.g_dirichlet));
+        check(fl_assemble(ctx.get(), m.m, &ff, &n, &fd, &fn, FL_OUT_SYSTEM, r.r), "fl_assemble");
+        check(fl_solve_system(ctx.get(), r.r, &o, sol.u.data(), FL_MEM_HOST, &it, &sol.final_relres),
+              "fl_solve_system");
+        sol.partition = detail::partition_of(mesh, r);
+    } else {
+        const femlite::index_t pin = opts.pin_node.value_or(0);
+        if (pin < 0 || pin >= mesh.num_nodes())
+            throw femlite::Error(femlite::ErrorCode::index_out_of_range, "pin_node out of range");
+        check(fl_assemble(ctx.get(), m.m, &ff, &n, &n, &fn, FL_OUT_STIFFNESS | FL_OUT_LOAD | FL_OUT_PARTITION, r.r),
+              "fl_assemble");
+        check(fl_solve_neumann(ctx.get(), m.m, r.r, pin, &o, sol.u.data(), FL_MEM_HOST, &it, &sol.final_relres),
+              "fl_solve_neumann");
+        sol.partition = detail::partition_of(mesh, r);
+    }
     sol.iterations = static_cast<femlite::index_t>(it);
-    sol.partition = detail::partition_of(mesh, r);
     return sol;
+}
+
+/// system.hpp:182-201 for any caller-supplied A and b: the partition, u0 = g at
+/// the Dirichlet nodes, b - A u0 (matvec's column order, sparse.hpp:129-141), on
+/// the GPU, bitwise.  g is sampled at every node on the host.
+inline femlite::DirichletSystem apply_dirichlet(const femlite::CscMatrix& a, std::span<const double> b,
+                                                const femlite::Mesh& mesh, const femlite::ScalarField& g,
+                                                Context& ctx = Context::default_context()) {
+    detail::MeshHandle m(ctx, mesh);
+    detail::ResultHandle r(ctx);
+    std::vector<double> gs;
+    fl_field gd = detail::none();
+    if (g) gd = detail::samples(gs = detail::sample_nodes(mesh, g));
+    check(fl_apply_dirichlet(ctx.get(), m.m, a.m, a.n, a.col_ptr.data(), a.row_idx.data(), a.values.data(),
+                             static_cast<int64_t>(b.size()), b.data(), FL_MEM_HOST, &gd, r.r),
+          "fl_apply_dirichlet");
+    const fl_sizes z = r.sizes();
+    femlite::DirichletSystem s;
+    s.u0 = r.array<double>(FL_U0, z.n);
+    s.b = r.array<double>(FL_B_MOD, z.n);
+    s.partition = detail::partition_of(mesh, r);
+    return s;
+}
+
+/// sparse.hpp:61-115 on the GPU (stable by (column, row), duplicates summed in
+/// their original order, exact-zero sums dropped), bitwise
+inline femlite::CscMatrix from_triplets(const femlite::Triplets& t, Context& ctx = Context::default_context()) {
+    if (t.i.size() != t.s.size() || t.j.size() != t.s.size())
+        throw femlite::Error(femlite::ErrorCode::shape_mismatch, "triplet arrays differ in length");
+    detail::ResultHandle r(ctx);
+    check(fl_from_triplets(ctx.get(), t.m, t.n, static_cast<int64_t>(t.size()), t.i.data(), t.j.data(),
+                           t.s.data(), FL_MEM_HOST, r.r),
+          "fl_from_triplets");
+    return r.matrix(t.m);
+}
+
+/// sparse.hpp:186-198 on the GPU, bitwise
+inline std::vector<double> accumulate(std::span<const femlite::index_t> idx, std::span<const double> vals,
+                                      femlite::index_t size, Context& ctx = Context::default_context()) {
+    if (idx.size() != vals.size())
+        throw femlite::Error(femlite::ErrorCode::shape_mismatch, "accumulate: index/value lengths differ");
+    std::vector<double> out(static_cast<std::size_t>(size > 0 ? size : 0));
+    check(fl_accumulate(ctx.get(), static_cast<int64_t>(idx.size()), idx.data(), vals.data(), size,
+                        out.empty() ? nullptr : out.data(), FL_MEM_HOST),
+          "fl_accumulate");
+    return out;
 }
 
 /// sparse.hpp:159 (strictly increasing index sets, validated on the GPU)

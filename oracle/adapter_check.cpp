@@ -57,6 +57,11 @@ femlite::Mesh jitter(const femlite::Mesh& m, double amp, unsigned seed) {
     return femlite::make_mesh(m.dim(), nodes, m.elems(), m.bd_flags());
 }
 
+// FaceList (mesh.hpp:101-109) element by element
+bool same_faces(const femlite::FaceList& a, const femlite::FaceList& b) {
+    return a.dim == b.dim && a.faces == b.faces && a.parent_elem == b.parent_elem && a.local_face == b.local_face;
+}
+
 void run(const char* name, const femlite::Mesh& mesh) {
     using namespace femlite;
     const double pi = std::numbers::pi;
@@ -72,10 +77,10 @@ void run(const char* name, const femlite::Mesh& mesh) {
     expect(same(b, femlite_b200::assemble_load(mesh, f)), "assemble_load", name);
     const BoundaryPartition p = partition_boundary(mesh);
     const BoundaryPartition q = femlite_b200::partition_boundary(mesh);
-    expect(p.dirichlet_nodes == q.dirichlet_nodes && p.free_nodes == q.free_nodes &&
-               p.dirichlet_faces.size() == q.dirichlet_faces.size() &&
-               p.neumann_faces.size() == q.neumann_faces.size(),
-           "partition_boundary", name);
+    expect(p.dirichlet_nodes == q.dirichlet_nodes && p.free_nodes == q.free_nodes, "partition_boundary nodes",
+           name);
+    expect(same_faces(p.dirichlet_faces, q.dirichlet_faces), "partition_boundary dirichlet_faces", name);
+    expect(same_faces(p.neumann_faces, q.neumann_faces), "partition_boundary neumann_faces", name);
     expect(same(apply_neumann(b, mesh, gn), femlite_b200::apply_neumann(b, mesh, gn)), "apply_neumann",
            name);
     if (p.dirichlet_faces.size() > 0) {
@@ -106,6 +111,48 @@ void run(const char* name, const femlite::Mesh& mesh) {
         }
         expect(worst <= 1e-7 * scale, "solve_poisson u (1e-7 relative)", name);
         expect(std::abs(ref_sol.iterations - gpu_sol.iterations) <= 2, "solve_poisson iterations", name);
+        // apply_dirichlet with an A and b that are not the assembled ones (system.hpp:182-201)
+        CscMatrix a2 = a;
+        for (double& v : a2.values) v = 2.0 * v;
+        std::vector<double> b2(bn.size());
+        for (std::size_t k = 0; k < b2.size(); ++k) b2[k] = 0.5 * bn[k] - 1.0 / double(k + 3);
+        const DirichletSystem d2 = apply_dirichlet(a2, b2, mesh, g);
+        const DirichletSystem q2 = femlite_b200::apply_dirichlet(a2, b2, mesh, g);
+        expect(same(d2.u0, q2.u0) && same(d2.b, q2.b), "apply_dirichlet(2A, b')", name);
+        expect(same_faces(d2.partition.dirichlet_faces, q2.partition.dirichlet_faces) &&
+                   d2.partition.free_nodes == q2.partition.free_nodes,
+               "apply_dirichlet partition", name);
+        // ... and with A from from_triplets of a scrambled COO (duplicates, cancellations)
+        Triplets t(a.m, a.n);
+        for (index_t c = 0; c < a.n; ++c)
+            for (index_t k = a.col_ptr[c]; k < a.col_ptr[c + 1]; ++k) {
+                const index_t r = a.row_idx[k];
+                t.push(r, c, a.values[k] * 0.75);
+                t.push((r * 7 + c) % a.m, (c * 3 + 1) % a.n, 1.0 / double(k + 1));
+                t.push((r * 7 + c) % a.m, (c * 3 + 1) % a.n, -1.0 / double(k + 1));
+            }
+        const CscMatrix at = from_triplets(t);
+        expect(at == femlite_b200::from_triplets(t), "from_triplets", name);
+        const DirichletSystem r3 = apply_dirichlet(at, b2, mesh, g);
+        const DirichletSystem q3 = femlite_b200::apply_dirichlet(at, b2, mesh, g);
+        expect(same(r3.u0, q3.u0) && same(r3.b, q3.b), "apply_dirichlet(from_triplets A, b')", name);
+        // accumulate (sparse.hpp:186-198)
+        std::vector<index_t> idx;
+        std::vector<double> vals;
+        for (std::size_t k = 0; k < t.size(); ++k) {
+            idx.push_back(t.i[k]);
+            vals.push_back(t.s[k]);
+        }
+        expect(same(accumulate(idx, vals, a.m), femlite_b200::accumulate(idx, vals, a.m)), "accumulate", name);
+        // dense_direct is rejected explicitly
+        SolveOptions dd;
+        dd.method = SolveMethod::dense_direct;
+        try {
+            femlite_b200::solve_poisson(mesh, pb, dd);
+            expect(false, "dense_direct rejected", name);
+        } catch (const Error& e) {
+            expect(e.code() == ErrorCode::invalid_parameter, "dense_direct rejected", name);
+        }
         // general submatrix
         std::vector<index_t> rows, cols;
         for (index_t k = 0; k < a.m; k += 2) rows.push_back(k);
@@ -140,6 +187,27 @@ int main() {
     run("unit_cube:4", cu);
     run("unit_cube:4 jittered", jitter(cu, 0.04, 13));
     run("unit_cube:3 mixed", set_boundary_flags(generate_mesh(MeshShape::unit_cube, 3), mixed));
+    // pure-Neumann solve_poisson (solver.hpp:253-276): no Dirichlet face
+    {
+        const Mesh pn = set_boundary_flags(generate_mesh(MeshShape::unit_square, 10), [](const Point&) { return 2; });
+        const double pi = std::numbers::pi;
+        const PoissonProblem pb{[pi](const Point& p) { return std::cos(pi * p[0]) * std::cos(pi * p[1]); }, {},
+                                [](const Point& p) { return p[0] - 0.5; }};
+        for (int pin : {0, 7}) {
+            SolveOptions so;
+            so.pin_node = pin;
+            const Solution rs = femlite::solve_poisson(pn, pb, so);
+            const Solution gs = femlite_b200::solve_poisson(pn, pb, so);
+            double worst = 0.0, scale = 1.0;
+            for (std::size_t k = 0; k < rs.u.size(); ++k) {
+                worst = std::max(worst, std::abs(rs.u[k] - gs.u[k]));
+                scale = std::max(scale, std::abs(rs.u[k]));
+            }
+            expect(worst <= 1e-7 * scale, "solve_poisson pure-Neumann u (1e-7 relative)", "unit_square:10 neumann");
+            expect(same_faces(rs.partition.neumann_faces, gs.partition.neumann_faces),
+                   "solve_poisson pure-Neumann partition", "unit_square:10 neumann");
+        }
+    }
     // errors surface as femlite::Error with the reference's code
     try {
         const Mesh robin = set_boundary_flags(generate_mesh(MeshShape::unit_square, 2),

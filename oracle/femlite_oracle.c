@@ -762,6 +762,32 @@ int fo_partition_boundary(int dim, int32_t n_nodes, int32_t n_elems, const int32
     return FO_OK;
 }
 
+/* boundary_faces (mesh.hpp:222-246): faces with flag == value, face-major
+ * (all local faces 0 over t, then 1, ...), vertices in kTriFaces / kTetFaces
+ * order, with the parent element and the local face. */
+int fo_boundary_faces(int dim, int32_t n_elems, const int32_t* elems, const int8_t* flags, int value,
+                      int32_t* n_faces, int32_t** faces, int32_t** parent, int32_t** local) {
+    const int d = dim, nv = dim + 1;
+    if (value < 1 || value > 3) return E_INVALID_FLAG_VALUE;
+    int32_t n = 0;
+    for (size_t k = 0; flags && k < (size_t)n_elems * nv; ++k) n += flags[k] == value;
+    *faces = xmalloc(sizeof(int32_t) * (size_t)(n ? n * d : 1));
+    *parent = xmalloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    *local = xmalloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    int32_t q = 0;
+    for (int lf = 0; lf <= d && flags; ++lf)
+        for (int32_t t = 0; t < n_elems; ++t) {
+            if (flags[(size_t)t * nv + lf] != value) continue;
+            const int32_t* v = elems + (size_t)t * nv;
+            for (int k = 0; k < d; ++k) (*faces)[(size_t)q * d + k] = d == 2 ? v[kTriFaces[lf][k]] : v[kTetFaces[lf][k]];
+            (*parent)[q] = t;
+            (*local)[q] = lf;
+            ++q;
+        }
+    *n_faces = n;
+    return FO_OK;
+}
+
 /* system.hpp:182-201 */
 int fo_apply_dirichlet(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                        const int32_t* elems, const int8_t* flags, const fo_csc* a,

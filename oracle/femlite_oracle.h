@@ -91,6 +91,9 @@ int fo_partition_boundary(int dim, int32_t n_nodes, int32_t n_elems, const int32
                           const int8_t* flags, int32_t* n_dir, int32_t** dir_nodes,
                           int32_t* n_free, int32_t** free_nodes, int32_t* n_dir_faces,
                           int32_t* n_neu_faces);
+/* boundary_faces (mesh.hpp:222-246), arrays malloc'ed (fo_free) */
+int fo_boundary_faces(int dim, int32_t n_elems, const int32_t* elems, const int8_t* flags, int value,
+                      int32_t* n_faces, int32_t** faces, int32_t** parent, int32_t** local);
 /* system.hpp:182-201 (g of kind NONE is rejected like calling an empty
  * std::function; SAMPLES = g at every node, used only at Dirichlet nodes) */
 int fo_apply_dirichlet(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,

@@ -336,6 +336,28 @@ def partition_boundary(dim, nodes, elems, flags, which: str = "oracle"):
             ndf.value, nnf.value)
 
 
+def boundary_faces(dim, nodes, elems, flags, value: int, which: str = "oracle"):
+    """boundary_faces(mesh, value) (mesh.hpp:222-246) -> (faces [n, dim], parent_elem, local_face)."""
+    L = lib(which)
+    nodes, elems, flags = _arr_f64(nodes), _arr_i32(elems), _arr_i8(flags)
+    nn, ne = nodes.shape[0], elems.shape[0]
+    n = C.c_int32()
+    fa, pa, la = _i32p(), _i32p(), _i32p()
+    if which == "oracle":
+        _check(L.fo_boundary_faces(C.c_int(dim), C.c_int32(ne), _p(elems, _i32p), _p(flags, _i8p),
+                                   C.c_int(value), C.byref(n), C.byref(fa), C.byref(pa), C.byref(la)))
+        free = L.fo_free
+    else:
+        _check(L.ref_boundary_faces(C.c_int(dim), C.c_int32(nn), C.c_int32(ne), _p(nodes, _f64p),
+                                    _p(elems, _i32p), _p(flags, _i8p), C.c_int(value), C.byref(n),
+                                    C.byref(fa), C.byref(pa), C.byref(la)), "ref")
+        free = L.ref_free
+    free.argtypes = [C.c_void_p]
+    k = n.value
+    return (_take(fa, k * dim, np.int32, free).reshape(k, dim), _take(pa, k, np.int32, free),
+            _take(la, k, np.int32, free))
+
+
 def apply_dirichlet(dim, nodes, elems, flags, a: Csc, b, g_kind, g_value=0.0, g_samples=None,
                     which: str = "oracle"):
     L = lib(which)

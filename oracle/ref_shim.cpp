@@ -271,6 +271,20 @@ int ref_partition_boundary(int dim, int32_t n_nodes, int32_t n_elems, const doub
     });
 }
 
+int ref_boundary_faces(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
+                       const int32_t* elems, const int8_t* flags, int value, int32_t* n_faces,
+                       int32_t** faces, int32_t** parent, int32_t** local) {
+    return guarded([&] {
+        const Mesh m = mesh_from(dim, n_nodes, n_elems, nodes, elems, flags);
+        const FaceList f = boundary_faces(m, value);
+        *n_faces = static_cast<int32_t>(f.size());
+        *faces = dup(f.faces);
+        *parent = dup(f.parent_elem);
+        std::vector<int32_t> lf(f.local_face.begin(), f.local_face.end());
+        *local = dup(lf);
+    });
+}
+
 int ref_apply_dirichlet(int dim, int32_t n_nodes, int32_t n_elems, const double* nodes,
                         const int32_t* elems, const int8_t* flags, const int32_t* col_ptr,
                         const int32_t* row_idx, const double* values, const double* b,

@@ -16,9 +16,10 @@ Public API mirrors femlite (/root/reference/proj/include/femlite/):
 All compute runs in libfemlite_b200.so (hand-written sm_100a kernels behind
 the C-ABI of include/femlite_b200.h); importing does not touch the GPU.
 """
-from .api import (AssemblyResult, AssemblyStrategy, BoundaryPartition, CgResult, CscMatrix,
+from .api import (AssemblyResult, AssemblyStrategy, BoundaryPartition, CgResult, CscMatrix, FaceList,
                   DirichletSystem, PoissonSystem, Solution, assemble, assemble_blockwise,
-                  assemble_load, assemble_system, apply_neumann, cg_solve, from_triplets, matvec,
+                  accumulate, apply_dirichlet, assemble_load, assemble_system, apply_neumann, cg_solve,
+                  from_triplets, matvec,
                   partition_boundary,
                   poisson_system, run, solve_poisson, submatrix)
 from .context import Context
@@ -30,9 +31,10 @@ from .mesh import (Mesh, MeshShape, boundary_face_mask, classifier_dirichlet, cl
                    set_boundary_flags)
 
 __all__ = [
-    "AssemblyResult", "AssemblyStrategy", "BoundaryPartition", "CgResult", "Context", "CscMatrix",
+    "AssemblyResult", "AssemblyStrategy", "BoundaryPartition", "CgResult", "Context", "CscMatrix", "FaceList",
     "DirichletSystem", "Error", "ErrorCode", "Mesh", "MeshShape", "PoissonSystem", "assemble",
-    "assemble_blockwise", "assemble_load", "assemble_system", "apply_neumann",
+    "accumulate", "apply_dirichlet", "assemble_blockwise", "assemble_load", "assemble_system",
+    "apply_neumann",
     "boundary_face_mask", "classifier_dirichlet", "classifier_lshape", "classifier_mixed",
     "classifier_neumann", "flag_generated", "generate_mesh", "make_mesh", "partition_boundary",
     "poisson_system", "run", "set_boundary_flags", "submatrix", "cg_solve", "matvec", "solve_poisson",

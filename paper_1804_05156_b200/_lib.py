@@ -19,7 +19,8 @@ MEM_HOST, MEM_DEVICE = 0, 1
 FIELD_NONE, FIELD_CONST, FIELD_SINSIN, FIELD_X, FIELD_XYZ, FIELD_SAMPLES, FIELD_COEF_C5 = 0, 1, 2, 3, 4, 6, 7
 OUT_STIFFNESS, OUT_LOAD, OUT_PARTITION, OUT_SYSTEM, REPLAN = 1, 2, 4, 8, 16
 (A_COL_PTR, A_ROW_IDX, A_VALUES, B, U0, B_MOD, DIR_NODES, FREE_NODES,
- AFF_COL_PTR, AFF_ROW_IDX, AFF_VALUES, B_F) = range(12)
+ AFF_COL_PTR, AFF_ROW_IDX, AFF_VALUES, B_F, DIR_FACES, DIR_FACE_ELEM, DIR_FACE_LOCAL,
+ NEU_FACES, NEU_FACE_ELEM, NEU_FACE_LOCAL) = range(18)
 
 FL_ERR_ARGUMENT, FL_ERR_CUDA, FL_ERR_NO_DEVICE, FL_ERR_OUT_OF_MEMORY, FL_ERR_UNSUPPORTED = 100, 101, 102, 103, 104
 
@@ -45,6 +46,9 @@ SIGNATURES = {
     "fl_cg_solve": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "fl_solve_system": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
     "fl_from_triplets": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp, C.c_int, _vp]),
+    "fl_apply_dirichlet": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, C.c_int64, _vp, C.c_int,
+                                     _vp, _vp]),
+    "fl_accumulate": (C.c_int, [_vp, C.c_int64, _vp, _vp, C.c_int32, _vp, C.c_int]),
     "fl_solve_neumann": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp, _vp, C.c_int, _vp, _vp]),
     "fl_matvec": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_int]),
     "fl_boundary_faces_copy": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int]),

@@ -55,11 +55,35 @@ class CscMatrix:  # sparse.hpp:50-59
 
 
 @dataclass
-class BoundaryPartition:  # system.hpp:39-44 (face lists summarised by their counts)
+class FaceList:  # mesh.hpp:101-109
+    dim: int
+    faces: np.ndarray        # [M, dim] vertices in kTriFaces / kTetFaces order
+    parent_elem: np.ndarray  # [M]
+    local_face: np.ndarray   # [M]
+
+    def size(self) -> int:
+        return int(self.parent_elem.shape[0])
+
+    def __eq__(self, other) -> bool:
+        return (self.dim == other.dim and np.array_equal(self.faces, other.faces)
+                and np.array_equal(self.parent_elem, other.parent_elem)
+                and np.array_equal(self.local_face, other.local_face))
+
+
+@dataclass
+class BoundaryPartition:  # system.hpp:39-44
     dirichlet_nodes: np.ndarray
     free_nodes: np.ndarray
-    n_dirichlet_faces: int = 0
-    n_neumann_faces: int = 0
+    dirichlet_faces: FaceList
+    neumann_faces: FaceList
+
+    @property
+    def n_dirichlet_faces(self) -> int:
+        return self.dirichlet_faces.size()
+
+    @property
+    def n_neumann_faces(self) -> int:
+        return self.neumann_faces.size()
 
 
 @dataclass
@@ -203,11 +227,21 @@ class AssemblyResult:
         n = s.n_free_cols if which == _lib.B_F else s.n
         return self.array(which, np.float64, n)
 
+    def face_list(self, dirichlet: bool) -> FaceList:
+        """boundary_faces(mesh, 1 | 2) as produced on the GPU (mesh.hpp:222-246)."""
+        s = self.sizes()
+        d = getattr(self, "_dim", 2)
+        n = s.n_dir_faces if dirichlet else s.n_neu_faces
+        w = (_lib.DIR_FACES, _lib.DIR_FACE_ELEM, _lib.DIR_FACE_LOCAL) if dirichlet else \
+            (_lib.NEU_FACES, _lib.NEU_FACE_ELEM, _lib.NEU_FACE_LOCAL)
+        return FaceList(d, self.array(w[0], np.int32, n * d).reshape(n, d),
+                        self.array(w[1], np.int32, n), self.array(w[2], np.int32, n))
+
     def partition(self) -> BoundaryPartition:
         s = self.sizes()
         return BoundaryPartition(self.array(_lib.DIR_NODES, np.int32, s.n_dir),
                                  self.array(_lib.FREE_NODES, np.int32, s.n_free),
-                                 s.n_dir_faces, s.n_neu_faces)
+                                 self.face_list(True), self.face_list(False))
 
     def __del__(self):
         if sys.is_finalizing():  # the CUDA runtime may already be gone; the OS reclaims
@@ -235,6 +269,7 @@ def run(mesh: Mesh, what: int, f=None, coef=None, g_dirichlet=None, g_neumann=No
                                       C.byref(fn), what, res.handle), "fl_assemble")
     res._keep = (k1, k2, k3, k4)
     res._rows = mesh.num_nodes()
+    res._dim = mesh.dim
     res._what = what
     return res
 
@@ -301,20 +336,38 @@ def poisson_system(mesh: Mesh, f, g_dirichlet, g_neumann=None, coef=None,
 
 
 def apply_dirichlet(a: CscMatrix, b, mesh: Mesh, g, ctx: Optional[Context] = None) -> DirichletSystem:
-    """system.hpp:182 for A = assemble_blockwise(mesh), b = the load of the same
-    mesh (the solve_poisson use).  The lift b - A u0 is computed on the GPU with
-    the transposed entries of A summed in the reference's order."""
-    n = mesh.num_nodes()
-    b = np.asarray(b, dtype=np.float64)
-    if a.m != n or a.n != n or b.shape[0] != n:
-        raise Error(ErrorCode.shape_mismatch, "apply_dirichlet: size mismatch")
-    r = run(mesh, _lib.OUT_SYSTEM, f=b_as_samples(mesh, b), g_dirichlet=g, ctx=ctx)
-    return DirichletSystem(r.vector(_lib.U0), r.vector(_lib.B_MOD), r.partition())
+    """system.hpp:182-201 for any A and b: partition_boundary(mesh), u0 = g at the
+    Dirichlet nodes, b - A u0 with A u0 summed in matvec's column order
+    (sparse.hpp:129-141) -- on the GPU, bitwise.  g: float | 'x' | 'xyz' |
+    'sinsin' | node samples | callable(x, y, z)."""
+    ctx = ctx or Context.default()
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    cp = np.ascontiguousarray(a.col_ptr, dtype=np.int32)
+    ri = np.ascontiguousarray(a.row_idx, dtype=np.int32)
+    va = np.ascontiguousarray(a.values, dtype=np.float64)
+    fd, keep = _field_struct(g, mesh, "dirichlet")
+    res = AssemblyResult(ctx)
+    _lib.check(_lib.lib().fl_apply_dirichlet(ctx.handle, mesh.device(ctx).handle, int(a.m), int(a.n),
+                                             cp.ctypes.data, ri.ctypes.data, va.ctypes.data, int(b.shape[0]),
+                                             b.ctypes.data, _lib.MEM_HOST, C.byref(fd), res.handle),
+               "fl_apply_dirichlet")
+    res._rows = mesh.num_nodes()
+    res._dim = mesh.dim
+    return DirichletSystem(res.vector(_lib.U0), res.vector(_lib.B_MOD), res.partition())
 
 
-def b_as_samples(mesh: Mesh, b):
-    raise Error(ErrorCode.invalid_parameter,
-                "apply_dirichlet with an arbitrary b is provided by assemble_system")
+def accumulate(idx, vals, size: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """sparse.hpp:186-198: out[k] = 0.0 + the vals with idx == k in their order (GPU, bitwise)."""
+    ctx = ctx or Context.default()
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    if idx.shape != vals.shape:
+        raise Error(ErrorCode.shape_mismatch, "accumulate: index/value lengths differ")
+    out = np.zeros(max(int(size), 0), dtype=np.float64)
+    _lib.check(_lib.lib().fl_accumulate(ctx.handle, int(idx.size), idx.ctypes.data if idx.size else None,
+                                        vals.ctypes.data if vals.size else None, int(size),
+                                        out.ctypes.data if out.size else None, _lib.MEM_HOST), "fl_accumulate")
+    return out
 
 
 def submatrix(a: CscMatrix, rows, cols, ctx: Optional[Context] = None) -> CscMatrix:

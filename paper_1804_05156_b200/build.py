@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfemlite_b200.so")
-SOURCES = ["fl_api.cu", "fl_kernels.cu", "fl_columns2.cu", "fl_columns3.cu", "fl_boundary.cu", "fl_solver.cu", "fl_triplets.cu", "fl_text.cu"]
+SOURCES = ["fl_api.cu", "fl_kernels.cu", "fl_columns2.cu", "fl_columns3.cu", "fl_columns4.cu", "fl_boundary.cu", "fl_solver.cu", "fl_triplets.cu", "fl_text.cu"]
 HEADERS = ["fl_internal.cuh", "fl_scan.cuh", "fl_geometry.cuh", "fl_kernels.cuh", "fl_pow10.cuh"]
 
 NVCC_FLAGS = [

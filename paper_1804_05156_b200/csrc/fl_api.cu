@@ -119,6 +119,14 @@ static int rerun_general(fl_result* res, fl_result_ext* x) {
     fl_mesh* mesh = x->last_mesh;
     ColParams p = x->last;
     uint32_t* counters = res->counters.as<uint32_t>();
+    if (res->v4_used) {
+        // the label-space pass overflowed: the general kernel works on the
+        // id-space plan and writes every output in node order itself
+        if (!mesh->planned || mesh->stats_stale) FL_TRY(fl_mesh_plan(ctx, mesh));
+        p.inc_ptr = mesh->inc_ptr.as<int32_t>();
+        p.inc = mesh->inc.as<uint32_t>();
+        res->v4_used = false;
+    }
     // the general kernel may need the plan's full output bound
     const size_t cap = (size_t)std::max<int64_t>(mesh->nnz_bound, 1);
     if (p.want_a) {
@@ -458,7 +466,25 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     ctx->plan_timed = false;
     ctx->kernel_timed = false;
     const bool need_plan = what & (FL_OUT_STIFFNESS | FL_OUT_LOAD);
-    if (need_plan && (replan || !mesh->planned) && mesh->ever_planned) {
+    const char* kern = std::getenv("FL_KERNEL");
+    const char kk = kern ? kern[0] : '0';
+    // the label-space pipeline (fl_columns4.cu) takes whole meshes without
+    // Neumann data whose valence fits its kernel; FL_V4=0 forces the id-space one
+    const char* v4env = std::getenv("FL_V4");
+    const bool neu_data = (what & FL_OUT_LOAD) && mesh->has_flags && g_neumann &&
+                          g_neumann->kind != FL_FIELD_NONE;
+    bool use_v4 = need_plan && kk == '0' && !(v4env && v4env[0] == '0') && mesh->col_begin == 0 &&
+                  mesh->col_end == mesh->n_nodes && mesh->n_nodes > 0 && mesh->n_elems > 0 &&
+                  mesh->lp.ok && !neu_data;
+    if (use_v4 && (replan || !mesh->lp.planned)) {
+        // a re-plan runs asynchronously with the previous bounds (fl_result_sizes
+        // refreshes them and reruns on the general kernel if they were exceeded)
+        FL_TRY(v4_plan(ctx, mesh, !mesh->lp.ever));
+        ctx->plan_timed = true;
+        if (!mesh->lp.ok) use_v4 = false;  // valence above the kernel's lanes
+    }
+    if (use_v4) {
+    } else if (need_plan && (replan || !mesh->planned) && mesh->ever_planned) {
         // Rebuild asynchronously: allocation and kernel choice use the previous
         // plan's bounds; fl_result_sizes refreshes the statistics and, should the
         // new topology exceed them, re-runs the column pass on the general kernel.
@@ -474,6 +500,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
     fl_result_ext* x = ext_of(res);
     res->sizes_valid = false;
+    res->v4_used = false;
     res->what = what;
     const int32_t N = mesh->n_nodes;
     const int32_t C0 = mesh->col_begin, NC = mesh->col_end - mesh->col_begin;
@@ -498,13 +525,11 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     // Output capacity.  The tiled / register kernels keep at most 12 (2-D) /
     // 24 (3-D) distinct rows per column (else they flag the general kernel,
     // which re-sizes to the plan's bound in rerun_general): size for that.
-    const char* kern = std::getenv("FL_KERNEL");
-    const char kk = kern ? kern[0] : '0';
     const int64_t fast_rows = mesh->dim == 2 ? 12 : 24;
-    const int64_t bound = std::max<int64_t>(mesh->nnz_bound, 1);
+    const int64_t bound = std::max<int64_t>(use_v4 ? mesh->lp.nnz_bound : mesh->nnz_bound, 1);
     // columns above the register kernel's valence go to the hybrid pass, sized
     // by the plan's bound
-    const bool hyb = mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc);
+    const bool hyb = !use_v4 && mesh->max_inc > columns3_lanes(mesh->dim, mesh->max_inc);
     const size_t cap = (size_t)(kk == '1' || hyb ? bound
                                                  : std::min<int64_t>(bound, fast_rows * std::max(NC, 1)));
     uint32_t* counters = res->counters.as<uint32_t>();
@@ -532,7 +557,10 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         FL_TRY(res->arr[FL_AFF_VALUES].ensure(sizeof(double) * cap));
         FL_CUDA(cudaMemsetAsync(res->arr[FL_AFF_COL_PTR].p, 0, sizeof(int32_t), s));
     }
-    if (want_p) FL_TRY(launch_partition(ctx, mesh, res));
+    if (want_p) {
+        FL_TRY(launch_partition(ctx, mesh, res));
+        FL_TRY(launch_face_lists(ctx, mesh, res));
+    }
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[2], s));
 
     if (want_a || want_b) {
@@ -594,7 +622,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         // a cached plan used again: sort its segments once, the register kernel
         // then skips its key sort on this and every later assembly of the mesh
         const char* ks = std::getenv("FL_KEYSORT");
-        if (kk == '0' && !ctx->plan_timed && !(ks && ks[0] == '0')) {
+        if (kk == '0' && !use_v4 && !ctx->plan_timed && !(ks && ks[0] == '0')) {
             if (!mesh->inc_sorted) FL_TRY(launch_inc_sort(ctx, mesh));
             p.keys_sorted = true;
         }
@@ -606,7 +634,10 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
             // carries the Dirichlet lift; v1 (general) is the fallback.
             // FL_KERNEL=1|2|3 forces one (3 = v3 with in-kernel geometry).
             const char k = kk;
-            if (k == '1') {
+            if (use_v4) {
+                FL_TRY(v4_columns(ctx, mesh, p, res));
+                x->last = p;
+            } else if (k == '1') {
                 FL_TRY(launch_inc_sort(ctx, mesh));
                 FL_TRY(launch_columns(ctx, mesh->dim, p));
             } else if (k == '2' || (k == '3' && (p.need_lift || (p.has_neumann && p.g_neu.kind != FL_FIELD_NONE)))) {
@@ -642,9 +673,14 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
         hn[0] = hn[1] = hn[2] = hn[3] = hn[4] = 0;
         fl_mesh* lm = x->last_valid ? x->last_mesh : nullptr;
         unsigned long long* hst = reinterpret_cast<unsigned long long*>(h + CNT_WORDS + 16);
-        if (lm && lm->stats_stale)
+        if (lm && lm->stats_stale && !res->v4_used)
             FL_CUDA(cudaMemcpyAsync(hst, lm->stats.p, sizeof(unsigned long long) * 4,
                                     cudaMemcpyDeviceToHost, s));
+        // the label plan's statistics and error word (v4 re-plans run asynchronously)
+        const bool v4s = lm && res->v4_used && lm->lp.stale;
+        unsigned long long* h4 = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->pinned) + 256);
+        if (v4s)
+            FL_CUDA(cudaMemcpyAsync(h4, lm->lp.misc.p, sizeof(unsigned long long) * 5, cudaMemcpyDeviceToHost, s));
         const bool sharded_sys = (res->what & FL_OUT_SYSTEM) && res->n != res->m;
         if (sharded_sys) {  // free nodes before / through the range
             const int32_t* fr = res->fidx.as<int32_t>() + (size_t)res->m + 1;
@@ -658,7 +694,15 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
                                     sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         FL_CUDA(cudaStreamSynchronize(s));
         bool replanned = false;
-        if (lm && lm->stats_stale) {  // an asynchronous re-plan ran with the old bounds
+        if (v4s) {
+            lm->lp.nnz_bound = (int64_t)h4[0];
+            lm->lp.max_inc = (int32_t)h4[1];
+            lm->lp.ok = lm->lp.max_inc <= v4_lanes(lm->dim);
+            lm->lp.stale = false;
+            replanned = true;
+            if ((uint32_t)(h4[4] >> 32) & DERR_INDEX) h[CNT_ERR] |= DERR_INDEX;
+        }
+        if (lm && lm->stats_stale && !res->v4_used) {  // an asynchronous re-plan ran with the old bounds
             lm->nnz_bound = (int64_t)hst[0];
             lm->max_inc = (int32_t)hst[1];
             lm->stats_stale = false;
@@ -746,13 +790,19 @@ static int64_t array_bytes(const fl_result* r, int which) {
     case FL_A_VALUES: return (r->what & FL_OUT_STIFFNESS) ? 8 * z.nnz : 0;
     case FL_B: return (r->what & FL_OUT_LOAD) ? 8 * (int64_t)z.n : 0;
     case FL_U0:
-    case FL_B_MOD: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n : 0;
+    case FL_B_MOD: return (r->what & (FL_OUT_SYSTEM | kWhatLift)) ? 8 * (int64_t)z.n : 0;
     case FL_DIR_NODES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_dir : 0;
     case FL_FREE_NODES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_free : 0;
     case FL_AFF_COL_PTR: return (r->what & FL_OUT_SYSTEM) ? 4 * ((int64_t)z.n_free_cols + 1) : 0;
     case FL_AFF_ROW_IDX: return (r->what & FL_OUT_SYSTEM) ? 4 * z.nnz_ff : 0;
     case FL_AFF_VALUES: return (r->what & FL_OUT_SYSTEM) ? 8 * z.nnz_ff : 0;
     case FL_B_F: return (r->what & FL_OUT_SYSTEM) ? 8 * (int64_t)z.n_free_cols : 0;
+    case FL_DIR_FACES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_dir_faces * r->dim : 0;
+    case FL_DIR_FACE_ELEM:
+    case FL_DIR_FACE_LOCAL: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_dir_faces : 0;
+    case FL_NEU_FACES: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_neu_faces * r->dim : 0;
+    case FL_NEU_FACE_ELEM:
+    case FL_NEU_FACE_LOCAL: return (r->what & FL_OUT_PARTITION) ? 4 * (int64_t)z.n_neu_faces : 0;
     }
     return -1;
 }
@@ -904,6 +954,119 @@ FL_API int fl_from_triplets(fl_ctx* ctx, int32_t m, int32_t n, int64_t count, co
         ds = x->stage.sub[2].as<double>();
     }
     return launch_from_triplets(ctx, m, n, count, di, dj, ds, res);
+}
+
+FL_API int fl_apply_dirichlet(fl_ctx* ctx, fl_mesh* mesh, int32_t m, int32_t n, const int32_t* col_ptr,
+                              const int32_t* row_idx, const double* values, int64_t b_len, const double* b,
+                              int mem, const fl_field* g, fl_result* res) {
+    if (!ctx || !mesh || !res || !col_ptr) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (!field_ok(g)) return set_error(FL_ERR_ARGUMENT, "invalid field descriptor");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    if (mesh->col_begin != 0 || mesh->col_end != mesh->n_nodes)
+        return set_error(FL_ERR_UNSUPPORTED, "fl_apply_dirichlet needs the whole mesh (no column range)");
+    const cudaStream_t s = ctx->stream;
+    const int32_t N = mesh->n_nodes;
+    fl_result_ext* x = ext_of(res);
+    x->last_valid = false;
+    res->sizes_valid = false;
+    res->v4_used = false;
+    res->what = FL_OUT_PARTITION;
+    res->n = N;
+    res->m = N;
+    res->col_begin = 0;
+    res->dim = mesh->dim;
+    // partition_boundary first (system.hpp:185): Robin flags, then no Dirichlet faces
+    uint32_t* counters = res->counters.as<uint32_t>();
+    FL_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * CNT_WORDS, s));
+    const size_t n1 = (size_t)N + 1;
+    FL_TRY(res->is_dir.ensure(n1));
+    FL_TRY(res->is_neu.ensure(n1));
+    FL_TRY(res->fidx.ensure(sizeof(int32_t) * 2 * n1));
+    FL_TRY(res->arr[FL_DIR_NODES].ensure(sizeof(int32_t) * n1));
+    FL_TRY(res->arr[FL_FREE_NODES].ensure(sizeof(int32_t) * n1));
+    FL_TRY(launch_partition(ctx, mesh, res));
+    FL_TRY(launch_face_lists(ctx, mesh, res));
+    uint32_t* h = static_cast<uint32_t*>(ctx->pinned);
+    FL_CUDA(cudaMemcpyAsync(h, counters, sizeof(uint32_t) * CNT_WORDS, cudaMemcpyDeviceToHost, s));
+    FL_CUDA(cudaStreamSynchronize(s));
+    if (h[CNT_ERR] & DERR_INDEX) return set_error(FL_E_INDEX_OUT_OF_RANGE, "element vertex index out of range");
+    if (h[CNT_ERR] & DERR_FLAG) return set_error(FL_E_INVALID_FLAG_VALUE, "boundary flag not in {0,1,2,3}");
+    if (h[CNT_ERR] & DERR_ROBIN)
+        return set_error(FL_E_UNSUPPORTED_BOUNDARY_TYPE, "Robin boundary (flag 3) is not supported");
+    if (h[CNT_DIR_FACES] == 0)
+        return set_error(FL_E_NO_DIRICHLET_BOUNDARY, "mesh has no Dirichlet faces; use the pure-Neumann path");
+    if (m != N || n != N || b_len != N) return set_error(FL_E_SHAPE_MISMATCH, "apply_dirichlet: size mismatch");
+    if (N > 0 && (!b || !row_idx || !values)) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (!g || g->kind == FL_FIELD_NONE)  // the reference calls g: an empty std::function throws
+        return set_error(FL_ERR_ARGUMENT, "apply_dirichlet: g is empty");
+    FieldDesc gd;
+    FL_TRY(field_desc(ctx, g, N, x->stage.g_dir, &gd, "g_dirichlet"));
+    const int32_t* dcp = col_ptr;
+    const int32_t* dri = row_idx;
+    const double* dva = values;
+    const double* db = b;
+    if (mem != FL_MEM_DEVICE) {
+        const int64_t nnz = col_ptr[n];
+        FL_TRY(copy_in(ctx, x->stage.sub[0], col_ptr, sizeof(int32_t) * ((size_t)n + 1), FL_MEM_HOST));
+        FL_TRY(copy_in(ctx, x->stage.sub[1], row_idx, sizeof(int32_t) * (size_t)nnz, FL_MEM_HOST));
+        FL_TRY(copy_in(ctx, x->stage.sub[2], values, sizeof(double) * (size_t)nnz, FL_MEM_HOST));
+        FL_TRY(copy_in(ctx, x->stage.sub[3], b, sizeof(double) * (size_t)N, FL_MEM_HOST));
+        dcp = x->stage.sub[0].as<int32_t>();
+        dri = x->stage.sub[1].as<int32_t>();
+        dva = x->stage.sub[2].as<double>();
+        db = x->stage.sub[3].as<double>();
+    }
+    FL_TRY(launch_dirichlet_lift(ctx, mesh, res, gd, dcp, dri, dva, db));
+    res->what = FL_OUT_PARTITION | kWhatLift;
+    return FL_OK;
+}
+
+FL_API int fl_accumulate(fl_ctx* ctx, int64_t count, const int32_t* idx, const double* vals, int32_t size,
+                         double* out, int mem) {
+    if (!ctx || (count > 0 && (!idx || !vals)) || (size > 0 && !out)) return set_error(FL_ERR_ARGUMENT, "null argument");
+    if (size < 0 || count < 0) return set_error(FL_E_SHAPE_MISMATCH, "accumulate: negative size");
+    FL_CUDA(cudaSetDevice(ctx->device));
+    fl_result* col = nullptr;
+    FL_TRY(fl_result_create(ctx, &col));
+    DevBuf zeros, dout;
+    int rc = zeros.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(count, 1));
+    if (!rc && count > 0) {
+        const cudaError_t e = cudaMemsetAsync(zeros.p, 0, sizeof(int32_t) * (size_t)count, ctx->stream);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    // the one-column from_triplets of (idx, 0, vals): stable by index, each
+    // index's values summed in their original order (sparse.hpp:61-115)
+    if (!rc) {
+        fl_result_ext* x = ext_of(col);
+        const int32_t* di = idx;
+        const double* dv = vals;
+        if (mem != FL_MEM_DEVICE) {
+            rc = copy_in(ctx, x->stage.sub[0], idx, sizeof(int32_t) * (size_t)count, FL_MEM_HOST);
+            if (!rc) rc = copy_in(ctx, x->stage.sub[2], vals, sizeof(double) * (size_t)count, FL_MEM_HOST);
+            di = x->stage.sub[0].as<int32_t>();
+            dv = x->stage.sub[2].as<double>();
+        }
+        if (!rc) rc = launch_from_triplets(ctx, size, 1, count, di, zeros.as<int32_t>(), dv, col);
+    }
+    fl_sizes z{};
+    if (!rc) rc = fl_result_sizes(col, &z);  // index_out_of_range surfaces here
+    double* target = out;
+    if (!rc && mem != FL_MEM_DEVICE) {
+        rc = dout.ensure(sizeof(double) * (size_t)std::max(size, 1));
+        target = dout.as<double>();
+    }
+    if (!rc && size > 0) rc = launch_scatter_column(ctx, col, size, target);
+    if (!rc && mem != FL_MEM_DEVICE && size > 0) {
+        const cudaError_t e = cudaMemcpyAsync(out, target, sizeof(double) * (size_t)size, cudaMemcpyDeviceToHost,
+                                              ctx->stream);
+        if (e != cudaSuccess) rc = set_error(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    cudaStreamSynchronize(ctx->stream);
+    zeros.release();
+    dout.release();
+    fl_result_destroy(col);
+    if (rc == FL_E_INDEX_OUT_OF_RANGE) set_error(rc, "accumulate: index out of range");
+    return rc;
 }
 
 FL_API int fl_solve_neumann(fl_ctx* ctx, fl_mesh* mesh, fl_result* res, int32_t pin,

@@ -382,6 +382,141 @@ __global__ void k_partition(int32_t n_nodes, const int8_t* __restrict__ is_dir,
 }
 
 // ===========================================================================
+// FaceLists of partition_boundary: boundary_faces(mesh, 1) and (mesh, 2)
+// (mesh.hpp:222-246): faces whose flag equals the value, face-major -- every
+// local face 0 over t ascending, then local face 1, ... -- each with its
+// vertices in kTriFaces / kTetFaces order (mesh.hpp:29-30), its element and
+// its local face.  Ordered compaction: per-block counts per (value, lf), an
+// exclusive scan over (lf, block), then each block writes its faces in order.
+// ===========================================================================
+constexpr int kFaceThreads = 256, kFaceItems = 16;  // elements per thread
+constexpr int kFaceBlockElems = kFaceThreads * kFaceItems;
+
+template <int D>
+__device__ __forceinline__ uint32_t elem_flags(const int8_t* __restrict__ flags, int64_t t) {
+    if constexpr (D == 3) return (uint32_t)__ldg(reinterpret_cast<const int32_t*>(flags) + t);
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) w |= (uint32_t)(uint8_t)__ldg(flags + t * 3 + k) << (8 * k);
+    return w;
+}
+
+// per-thread counts of its kFaceItems elements, 16-bit fields: word 0 = Dirichlet
+// lf 0..3, word 1 = Neumann lf 0..3
+template <int D>
+__device__ __forceinline__ void face_counts(const int8_t* __restrict__ flags, int32_t n_elems, int64_t t0,
+                                            uint64_t& cd, uint64_t& cn) {
+    cd = cn = 0;
+    for (int k = 0; k < kFaceItems; ++k) {
+        const int64_t t = t0 + k;
+        if (t >= n_elems) break;
+        const uint32_t w = elem_flags<D>(flags, t);
+        if (!w) continue;
+#pragma unroll
+        for (int lf = 0; lf <= D; ++lf) {
+            const int8_t f = (int8_t)(w >> (8 * lf));
+            if (f == 1) cd += 1ull << (16 * lf);
+            else if (f == 2) cn += 1ull << (16 * lf);
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFaceThreads) k_face_count(int32_t n_elems, const int8_t* __restrict__ flags,
+                                                            int32_t nblk, int32_t* __restrict__ bcnt) {
+    __shared__ uint64_t s[2][kFaceThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t cd, cn;
+    face_counts<D>(flags, n_elems, (int64_t)blockIdx.x * kFaceBlockElems + (int64_t)threadIdx.x * kFaceItems, cd, cn);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cd += __shfl_xor_sync(0xffffffffu, cd, o);
+        cn += __shfl_xor_sync(0xffffffffu, cn, o);
+    }
+    if (lane == 0) {
+        s[0][w] = cd;
+        s[1][w] = cn;
+    }
+    __syncthreads();
+    if (threadIdx.x <= 2 * D + 1) {  // (value, lf) = category
+        const int v = threadIdx.x / (D + 1), lf = threadIdx.x % (D + 1);
+        int32_t tot = 0;
+        for (int i = 0; i < kFaceThreads / 32; ++i) tot += (int32_t)((s[v][i] >> (16 * lf)) & 0xFFFFu);
+        // Dirichlet then Neumann; each lf-major over the blocks
+        bcnt[(int64_t)(v * (D + 1) + lf) * nblk + blockIdx.x] = tot;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFaceThreads) k_face_emit(int32_t n_elems, const int32_t* __restrict__ elems,
+                                                           const int8_t* __restrict__ flags, int32_t nblk,
+                                                           const int32_t* __restrict__ boff,
+                                                           int32_t* __restrict__ dfaces, int32_t* __restrict__ delem,
+                                                           int32_t* __restrict__ dlocal, int32_t* __restrict__ nfaces,
+                                                           int32_t* __restrict__ nelem, int32_t* __restrict__ nlocal) {
+    constexpr int NV = D + 1;
+    __shared__ uint64_t s[2][kFaceThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t t0 = (int64_t)blockIdx.x * kFaceBlockElems + (int64_t)threadIdx.x * kFaceItems;
+    uint64_t cd, cn;
+    face_counts<D>(flags, n_elems, t0, cd, cn);
+    // block-wide exclusive scan of the packed counts (fields never carry: <= 4096)
+    uint64_t id = cd, in = cn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t a = __shfl_up_sync(0xffffffffu, id, o), b = __shfl_up_sync(0xffffffffu, in, o);
+        if (lane >= o) {
+            id += a;
+            in += b;
+        }
+    }
+    if (lane == 31) {
+        s[0][w] = id;
+        s[1][w] = in;
+    }
+    __syncthreads();
+    uint64_t pd = id - cd, pn = in - cn;  // exclusive within the warp
+    for (int i = 0; i < w; ++i) {
+        pd += s[0][i];
+        pn += s[1][i];
+    }
+    if (!(cd | cn)) return;
+    int32_t pos[2][NV];
+#pragma unroll
+    for (int lf = 0; lf < NV; ++lf) {
+        pos[0][lf] = __ldg(boff + (int64_t)lf * nblk + blockIdx.x) + (int32_t)((pd >> (16 * lf)) & 0xFFFFu);
+        pos[1][lf] = __ldg(boff + (int64_t)(NV + lf) * nblk + blockIdx.x) + (int32_t)((pn >> (16 * lf)) & 0xFFFFu);
+    }
+    for (int k = 0; k < kFaceItems; ++k) {
+        const int64_t t = t0 + k;
+        if (t >= n_elems) break;
+        const uint32_t fw = elem_flags<D>(flags, t);
+        if (!fw) continue;
+#pragma unroll
+        for (int lf = 0; lf < NV; ++lf) {
+            const int8_t f = (int8_t)(fw >> (8 * lf));
+            if (f != 1 && f != 2) continue;
+            const int v = f - 1;
+            const int32_t q = pos[v][lf]++;
+            int32_t* faces = v ? nfaces : dfaces;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                // kTriFaces = {1,2},{2,0},{0,1}; kTetFaces = {1,3,2},{0,2,3},{0,3,1},{0,1,2}
+                int lv;
+                if constexpr (D == 2) lv = (lf + 1 + a) % 3;
+                else lv = (lf == 0) ? (a == 0 ? 1 : a == 1 ? 3 : 2)
+                          : (lf == 1) ? (a == 0 ? 0 : a == 1 ? 2 : 3)
+                          : (lf == 2) ? (a == 0 ? 0 : a == 1 ? 3 : 1)
+                                      : a;
+                faces[(int64_t)q * D + a] = __ldg(elems + t * NV + lv);
+            }
+            (v ? nelem : delem)[q] = (int32_t)t;
+            (v ? nlocal : dlocal)[q] = lf;
+        }
+    }
+}
+
+// ===========================================================================
 // column kernel
 // ===========================================================================
 constexpr int kHS = 256;           // per-warp slot table (distinct rows of a column)
@@ -934,7 +1069,14 @@ __global__ void k_selftest_div(int64_t n, const double* __restrict__ a, const do
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const Recip R = recip(b[i]);
-        q_fast[i] = div_by(a[i], R);
+        const double q1 = div_by(a[i], R);
+        // the batched form (div_fast + the all-or-nothing IEEE fallback) must agree
+        // bit for bit with div_by; a disagreement is reported as a finite sentinel
+        bool ok = divisor_ok(R);
+        double q2 = div_fast(a[i], R, ok);
+        if (!ok) q2 = __ddiv_rn(a[i], b[i]);
+        const bool same = __double_as_longlong(q1) == __double_as_longlong(q2);
+        q_fast[i] = same ? q1 : __longlong_as_double(0x7fefdeadbeefcafell);  // finite sentinel
         q_ieee[i] = __ddiv_rn(a[i], b[i]);
     }
 }
@@ -1398,6 +1540,109 @@ int launch_partition(fl_ctx* ctx, fl_mesh* mesh, fl_result* res) {
     k_partition<<<std::max(1, std::min(div_up(N, 256), ctx->sm_count * 8)), 256, 0, s>>>(
         N, is_dir, free_rank, res->fidx.as<int32_t>(), res->arr[FL_DIR_NODES].as<int32_t>(),
         res->arr[FL_FREE_NODES].as<int32_t>(), counters);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// apply_dirichlet (system.hpp:182-201) for a caller-supplied A and b:
+// u0 = g at Dirichlet nodes (0 elsewhere), b - matvec(A, u0) (sparse.hpp:129-141).
+// ---------------------------------------------------------------------------
+__global__ void k_dirichlet_u0(int32_t n, const int8_t* __restrict__ is_dir, FieldDesc g,
+                               const double* __restrict__ nodes, int dim, double* __restrict__ u0) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        u0[k] = is_dir[k] ? field_at_node(g, nodes, dim, k) : 0.0;
+}
+
+__global__ void k_sub(int32_t n, const double* __restrict__ b, const double* __restrict__ y,
+                      double* __restrict__ out) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        out[k] = b[k] - y[k];  // system.hpp:197-198
+}
+
+int launch_dirichlet_lift(fl_ctx* ctx, fl_mesh* mesh, fl_result* res, const FieldDesc& g,
+                          const int32_t* col_ptr, const int32_t* row_idx, const double* values,
+                          const double* b) {
+    const int32_t N = mesh->n_nodes;
+    const cudaStream_t s = ctx->stream;
+    FL_TRY(res->arr[FL_U0].ensure(sizeof(double) * ((size_t)N + 1)));
+    FL_TRY(res->arr[FL_B_MOD].ensure(sizeof(double) * ((size_t)N + 1)));
+    FL_TRY(res->v4[2].ensure(sizeof(double) * ((size_t)N + 1)));
+    double* u0 = res->arr[FL_U0].as<double>();
+    double* au0 = res->v4[2].as<double>();
+    const int grid = std::max(1, std::min(div_up(N, 256), ctx->sm_count * 8));
+    if (N > 0) {
+        k_dirichlet_u0<<<grid, 256, 0, s>>>(N, res->is_dir.as<int8_t>(), g, mesh->nodes.as<double>(), mesh->dim, u0);
+        count_launch(ctx);
+    }
+    FL_TRY(matvec_device(ctx, N, N, col_ptr, row_idx, values, u0, au0));
+    if (N > 0) {
+        k_sub<<<grid, 256, 0, s>>>(N, b, au0, res->arr[FL_B_MOD].as<double>());
+        count_launch(ctx);
+    }
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+// accumulate (sparse.hpp:186-198) from a one-column from_triplets result:
+// out = 0.0 everywhere, then out[row] = the entry (the duplicate sum in original
+// order; exactly-zero sums were dropped and stay 0.0, as 0.0 + ... gives there)
+__global__ void k_scatter_column(int32_t nnz_unused, const int32_t* __restrict__ col_ptr,
+                                 const int32_t* __restrict__ row_idx, const double* __restrict__ values,
+                                 double* __restrict__ out) {
+    (void)nnz_unused;
+    const int32_t nnz = col_ptr[1];
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x)
+        out[row_idx[k]] = values[k];
+}
+
+int launch_scatter_column(fl_ctx* ctx, fl_result* col, int32_t size, double* out) {
+    FL_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)size, ctx->stream));
+    k_scatter_column<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(0, col->arr[FL_A_COL_PTR].as<int32_t>(),
+                                                                 col->arr[FL_A_ROW_IDX].as<int32_t>(),
+                                                                 col->arr[FL_A_VALUES].as<double>(), out);
+    count_launch(ctx);
+    FL_CUDA(cudaGetLastError());
+    return FL_OK;
+}
+
+int launch_face_lists(fl_ctx* ctx, fl_mesh* mesh, fl_result* res) {
+    const cudaStream_t s = ctx->stream;
+    const int D = mesh->dim, NV = D + 1;
+    const int32_t NT = mesh->n_elems;
+    // capacity: at most one face per (t, lf)
+    const size_t cap = (size_t)std::max<int64_t>((int64_t)NT * NV, 1);
+    FL_TRY(res->arr[FL_DIR_FACES].ensure(sizeof(int32_t) * cap * D));
+    FL_TRY(res->arr[FL_DIR_FACE_ELEM].ensure(sizeof(int32_t) * cap));
+    FL_TRY(res->arr[FL_DIR_FACE_LOCAL].ensure(sizeof(int32_t) * cap));
+    FL_TRY(res->arr[FL_NEU_FACES].ensure(sizeof(int32_t) * cap * D));
+    FL_TRY(res->arr[FL_NEU_FACE_ELEM].ensure(sizeof(int32_t) * cap));
+    FL_TRY(res->arr[FL_NEU_FACE_LOCAL].ensure(sizeof(int32_t) * cap));
+    if (!mesh->has_flags || NT == 0) return FL_OK;  // no flags: empty lists
+    const int32_t nblk = (int32_t)(((int64_t)NT + kFaceBlockElems - 1) / kFaceBlockElems);
+    const int64_t ncat = (int64_t)NV * nblk;  // per value
+    FL_TRY(res->v4[3].ensure(sizeof(int32_t) * (size_t)(4 * ncat + 2)));
+    int32_t* bcnt = res->v4[3].as<int32_t>();
+    int32_t* boff = bcnt + 2 * ncat;
+    if (D == 2) k_face_count<2><<<nblk, kFaceThreads, 0, s>>>(NT, mesh->flags.as<int8_t>(), nblk, bcnt);
+    else k_face_count<3><<<nblk, kFaceThreads, 0, s>>>(NT, mesh->flags.as<int8_t>(), nblk, bcnt);
+    count_launch(ctx);
+    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(ncat)));
+    for (int v = 0; v < 2; ++v) {
+        const int32_t* src = bcnt + v * ncat;
+        FL_CUDA(launch_scan<int32_t>(
+            ncat, [src] __device__(int64_t i) { return (int64_t)src[i]; }, boff + v * ncat, ctx->scan_ws.p, s));
+        count_launch(ctx);
+    }
+    // launch_scan writes out[n] = total past each region's end: the Neumann
+    // region is scanned second, so the Dirichlet total it overwrote is not used
+    auto emit = D == 2 ? k_face_emit<2> : k_face_emit<3>;
+    emit<<<nblk, kFaceThreads, 0, s>>>(NT, mesh->elems.as<int32_t>(), mesh->flags.as<int8_t>(), nblk, boff,
+                                       res->arr[FL_DIR_FACES].as<int32_t>(), res->arr[FL_DIR_FACE_ELEM].as<int32_t>(),
+                                       res->arr[FL_DIR_FACE_LOCAL].as<int32_t>(), res->arr[FL_NEU_FACES].as<int32_t>(),
+                                       res->arr[FL_NEU_FACE_ELEM].as<int32_t>(),
+                                       res->arr[FL_NEU_FACE_LOCAL].as<int32_t>());
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;

@@ -80,6 +80,13 @@ struct ColParams {
     unsigned long long* ov_alloc;  // [2] running A / A(free,free) overflow-staging tops
     const double* nadd;  // Neumann shares per owned column (k_neumann_add), nullptr = none
     bool keys_sorted;    // the plan's segments are already in (j, t) order: no in-kernel sort
+    // label-space pipeline (v4, fl_columns4.cu): columns are labels; inc_ptr / inc
+    // are the label plan's; lel = elements with vertex labels; xl[label] = the
+    // node's coordinates and {node id, free rank or -1} in .w; vst[label] =
+    // {b, u0, b - A u0, 0}
+    const int32_t* lel;
+    const double4* xl;
+    double4* vst;
 };
 
 __device__ __forceinline__ int32_t free_base(const ColParams& p) {
@@ -124,6 +131,19 @@ int launch_from_triplets(fl_ctx* ctx, int32_t m, int32_t n, int64_t nz, const in
 int matvec_device(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr, const int32_t* row_idx,
                   const double* values, const double* x, double* y);
 size_t column_smem_bytes();
+// v4 (fl_columns4.cu)
+int v4_lanes(int dim);
+int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync);
+int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res);
+// FaceLists of partition_boundary (mesh.hpp:222-246) into res->faces
+int launch_face_lists(fl_ctx* ctx, fl_mesh* mesh, fl_result* res);
+// apply_dirichlet for a caller-supplied A and b (after launch_partition)
+int launch_dirichlet_lift(fl_ctx* ctx, fl_mesh* mesh, fl_result* res, const FieldDesc& g,
+                          const int32_t* col_ptr, const int32_t* row_idx, const double* values,
+                          const double* b);
+int launch_scatter_column(fl_ctx* ctx, fl_result* col, int32_t size, double* out);
+// fl_result::what bit of an fl_apply_dirichlet result (u0 and b - A u0 held)
+constexpr uint32_t kWhatLift = 1u << 8;
 int column_tile_width();
 
 }  // namespace fl

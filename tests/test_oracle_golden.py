@@ -173,3 +173,31 @@ def test_reference_blockwise_equals_triplets_on_binary_mesh():  # assembly_test.
     a = po.ref_assemble_strategy(d, nodes, elems, 2)
     b = po.ref_assemble_strategy(d, nodes, elems, 1)
     _csc_eq(a, b.col_ptr, b.row_idx, b.values)
+
+
+@needs_ref
+@pytest.mark.parametrize("path", GOLDEN)
+def test_oracle_face_lists_equal_reference(path):
+    """boundary_faces (mesh.hpp:222-246): the C restatement == the reference."""
+    g = np.load(path)
+    d, nodes, elems, flags = int(g["dim"]), g["nodes"], g["elems"], g["flags"]
+    for value in (1, 2):
+        a = po.boundary_faces(d, nodes, elems, flags, value)
+        b = po.boundary_faces(d, nodes, elems, flags, value, which="ref")
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+        assert a[0].shape[1] == d
+
+
+@needs_ref
+def test_oracle_accumulate_equals_reference():
+    """accumulate (sparse.hpp:186-198): order-sensitive sums and signed zeros."""
+    rng = np.random.default_rng(7)
+    idx = rng.integers(0, 50, size=4000).astype(np.int32)
+    vals = rng.standard_normal(4000) * 10.0 ** rng.integers(-8, 9, size=4000)
+    vals[::7] = -0.0
+    a = po.accumulate(idx, vals, 60)
+    b = po.accumulate(idx, vals, 60, which="ref")
+    assert a.tobytes() == b.tobytes()
+    with pytest.raises(po.OracleError):
+        po.accumulate(np.array([3, 70], np.int32), np.ones(2), 60, which="ref")
