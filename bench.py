@@ -359,6 +359,28 @@ def run_ours(args, rank: int, world: int):
     achieved = b_sl / (ms * 1e-3) / 1e9
     traffic = load_traffic(args.config) if world == 1 else None
 
+    # ---- optional verification gather to rank 0 (untimed): grouped NCCL
+    # send/recv of every shard into the global CSC (gloo: CPU tensors) ----
+    if args.dump_gather and world > 1:
+        from paper_1804_05156_b200.shard import ShardInfo, exclusive_offsets, gather_csc_to_root
+        info = ShardInfo(rank, world, c0, c1, gathered, exclusive_offsets(gathered))
+        tdev = f"cuda:{dev}" if os.environ.get("FL_BENCH_BACKEND", "nccl") == "nccl" else "cpu"
+        loc = []
+        for which, dt, cnt in ((_lib.A_COL_PTR, torch.int32, ncol_l + 1), (_lib.A_ROW_IDX, torch.int32, nnz_l),
+                               (_lib.A_VALUES, torch.float64, nnz_l)):
+            t = torch.empty(max(cnt, 1), dtype=dt, device=f"cuda:{dev}")
+            _lib.check(L.fl_result_copy(res.handle, which, t.data_ptr(), t.numel() * t.element_size(),
+                                        _lib.MEM_DEVICE))
+            loc.append(t[:cnt])
+        ctx.synchronize()  # the copies ran on the library's stream
+        loc = [t.to(tdev) for t in loc]
+        torch.cuda.synchronize()
+        out = gather_csc_to_root(info, *loc)
+        if rank == 0:
+            cp, ri, va = (x.cpu().numpy() for x in out)
+            np.savez(args.dump_gather, col_ptr=cp, row_idx=ri, values=va, config=args.config)
+            log(f"[bench] gathered the {world}-shard CSC on rank 0 -> {args.dump_gather}")
+
     # ---- e2e through the C-ABI with host buffers (pinned) ----
     e2e = None
     if not args.no_e2e:
@@ -397,8 +419,8 @@ def run_ours(args, rank: int, world: int):
                          "kernel": "the whole step (fl_assemble), SURVEY.md §8(d): achieved = B_SL / ms_per_step",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "algorithmic_bytes": b_sl,
-                         "traffic": traffic["step_dram_bytes"] if traffic else None,
-                         "traffic_source": traffic["source"] if traffic else None,
+                         "traffic": traffic.get("step_dram_bytes") if traffic else None,
+                         "traffic_source": traffic.get("source") if traffic else None,
                          "b_sys_frac": b_sys / (ms * 1e-3) / 1e9 / peak,
                          "dominant_kernel": {
                              "name": "k_columns4 (label-space column kernel)",
@@ -406,7 +428,7 @@ def run_ours(args, rank: int, world: int):
                              "compulsory_bytes": kern_bytes,
                              "achieved": kern_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None,
                              "frac": kern_bytes / (kern_ms * 1e-3) / 1e9 / peak if kern_ms > 0 else None,
-                             "traffic": traffic["kernel_dram_bytes"] if traffic else None}},
+                             "traffic": traffic.get("kernel_dram_bytes") if traffic else None}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_single": e2e["single_call"] if e2e else None,
@@ -539,6 +561,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--e2e-depth", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-gather", default=None,
+                    help="N>1: gather the sharded A to rank 0 after the timed loop (NCCL send/recv) and save it")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per k_columns launch (from profiles/), echoed into roofline")
     args = ap.parse_args()

@@ -294,6 +294,7 @@ FL_API int fl_mesh_set_elems(fl_ctx* ctx, fl_mesh* mesh, const int32_t* elems, i
     if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
     mesh->n_bfaces = -1;
     mesh->planned = false;
+    mesh->lp.planned = false;
     return copy_in(ctx, mesh->elems, elems, sizeof(int32_t) * (size_t)mesh->n_elems * (mesh->dim + 1),
                    mem);
 }
@@ -360,6 +361,9 @@ FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     mesh->bstage.release();
     mesh->bcnt.release();
     mesh->stats.release();
+    auto& lp = mesh->lp;
+    for (fl::DevBuf* b : {&lp.lab, &lp.ilab, &lp.lptr, &lp.linc, &lp.lel, &lp.lcnt, &lp.misc, &lp.cells, &lp.stage})
+        b->release();
     delete mesh;
     return FL_OK;
 }
@@ -437,6 +441,7 @@ FL_API int fl_result_destroy(fl_result* r) {
     r->colcnt.release();
     for (auto& b : r->erec) b.release();
     for (auto& b : r->hyb) b.release();
+    for (auto& b : r->v4) b.release();
     r->counters.release();
     fl_result_ext* x = ext_of(r);
     x->stage.f.release();

@@ -112,6 +112,15 @@ __global__ void __launch_bounds__(kElemThreads, D == 3 ? 8 : 6) k_elem_records(C
 #pragma unroll
                 for (int i = 0; i < NV; ++i) V[i] = __ldg(p.elems + (size_t)t * NV + i);
             }
+            // vertex ids outside [0, N): reported, never dereferenced
+            bool okv = true;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) okv = okv && (uint32_t)V[i] < (uint32_t)p.n_nodes;
+            if (!okv) {
+                atomicOr(p.err, DERR_INDEX);
+#pragma unroll
+                for (int i = 0; i < NV; ++i) V[i] = 0;
+            }
             ElemCol<D> ec;
             ec.load(p.nodes, V);
             double S[NV][NV];

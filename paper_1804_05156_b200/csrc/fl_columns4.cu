@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "fl_geometry.cuh"
@@ -145,6 +146,116 @@ k4_untouched(int32_t n_nodes, const int32_t* __restrict__ cnt, int32_t* __restri
     }
 }
 
+// ---- spatial labels (default): nodes bucketed by the Morton cell of their
+// coordinates (cells of ~64 nodes along a Z-curve over the bounding box), in any
+// element order -- C3 permutes its elements, so first-touch order is random there.
+__global__ void k4_bbox(int32_t n, int dim, const double* __restrict__ nodes, double* __restrict__ part) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        for (int d = 0; d < dim; ++d) {
+            const double x = __ldg(nodes + (size_t)v * dim + d);
+            lo[d] = fmin(lo[d], x);
+            hi[d] = fmax(hi[d], x);
+        }
+    __shared__ double s[6][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(kFull, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(kFull, hi[d], o));
+        }
+        if (lane == 0) {
+            s[d][w] = lo[d];
+            s[3 + d][w] = hi[d];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double r = s[threadIdx.x][0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][i]) : fmax(r, s[threadIdx.x][i]);
+        part[blockIdx.x * 6 + threadIdx.x] = r;
+    }
+}
+
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {  // 10 bits -> every third bit
+    x &= 0x3FFu;
+    x = (x | (x << 16)) & 0x030000FFu;
+    x = (x | (x << 8)) & 0x0300F00Fu;
+    x = (x | (x << 4)) & 0x030C30C3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+__device__ __forceinline__ uint32_t spread2(uint32_t x) {  // 15 bits -> every second bit
+    x &= 0x7FFFu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
+// cell of every node (Morton code of its quantised coordinates) and per-cell counts
+__global__ void k4_cell(int32_t n, int dim, int bits, int nparts, const double* __restrict__ nodes,
+                        const double* __restrict__ part, int32_t* __restrict__ cell, int32_t* __restrict__ ccnt) {
+    __shared__ double box[6];
+    if (threadIdx.x < 6) {
+        double r = part[threadIdx.x];
+        for (int b = 1; b < nparts; ++b) r = threadIdx.x < 3 ? fmin(r, part[b * 6 + threadIdx.x]) : fmax(r, part[b * 6 + threadIdx.x]);
+        box[threadIdx.x] = r;
+    }
+    __syncthreads();
+    const double side = (double)(1u << bits);
+    double sc[3];
+    for (int d = 0; d < 3; ++d) sc[d] = box[3 + d] > box[d] ? side / (box[3 + d] - box[d]) : 0.0;
+    const uint32_t qmax = (1u << bits) - 1;
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint32_t q[3] = {0, 0, 0};
+        for (int d = 0; d < dim; ++d) {
+            const double x = __ldg(nodes + (size_t)v * dim + d);
+            const double f = (x - box[d]) * sc[d];
+            q[d] = f > 0.0 ? min((uint32_t)f, qmax) : 0u;  // NaN coordinates land in cell 0
+        }
+        const uint32_t code = dim == 3 ? (spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2))
+                                       : (spread2(q[0]) | (spread2(q[1]) << 1));
+        cell[v] = (int32_t)code;
+        atomicAdd(ccnt + code, 1);
+    }
+}
+
+// label = the node's place in its cell's run (cursor seeded with the cell offsets)
+__global__ void k4_cell_scatter(int32_t n, const int32_t* __restrict__ cell, int32_t* __restrict__ cursor,
+                                int32_t* __restrict__ lab, int32_t* __restrict__ ilab) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int32_t lb = atomicAdd(cursor + __ldg(cell + v), 1);
+        lab[v] = lb;
+        ilab[lb] = v;
+    }
+}
+
+// incidence counts per node (label-free count pass of the spatial labelling)
+__global__ void __launch_bounds__(kP4Block)
+k4_count_plain(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
+               P4Misc* __restrict__ misc) {
+    const unsigned lower = (1u << (threadIdx.x & 31)) - 1;
+    const int64_t b0 = (int64_t)blockIdx.x * kP4Block * kP4Iters;
+    uint32_t err = 0;
+    for (int k = 0; k < kP4Iters; ++k) {
+        const int64_t e = b0 + (int64_t)k * kP4Block + threadIdx.x;
+        if (e - (threadIdx.x & 31) >= n_entries) break;  // warp-uniform
+        int32_t key = -1;
+        if (e < n_entries) {
+            const int32_t v = __ldg(elems + e);
+            if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
+            else key = v;
+        }
+        const unsigned g = __match_any_sync(kFull, key);
+        if (key >= 0 && (g & lower) == 0) atomicAdd(cnt + key, __popc(g));
+    }
+    if (__any_sync(kFull, err != 0) && (threadIdx.x & 31) == 0) atomicOr(&misc->err, DERR_INDEX);
+}
+
 // (j << 30 | t) keys into the label segments (cursor seeded with lptr) and the
 // elements with vertex labels.  U rounds of 32 consecutive entries per warp,
 // one warp iteration per block, blocks issued in element order (as k_inc_fill:
@@ -188,6 +299,71 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, const int32_
                 linc[p0] = (j << 30) | (uint32_t)t;
             }
         }
+    }
+}
+
+// ---- bucketed fill (large 2-D meshes, element order not spatial: C3).  The
+// direct fill scatters 4-byte keys over the whole incidence array there, each a
+// sector read-modify-write.  Instead: (1) partition (label, key) pairs into
+// buckets of 2^shift consecutive labels (block-local shared-memory ranks, one
+// global reservation per bucket per block: coalesced runs), writing lel on the
+// way; (2) fill from the staging in bucket order, so the live range of the
+// incidence array is one bucket's slice, resident in L2.
+constexpr int kB4Items = 16, kB4MaxBuckets = 1024;
+
+__global__ void __launch_bounds__(kP4Block)
+k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int shift, const int32_t* __restrict__ elems,
+                  const int32_t* __restrict__ lab, const int32_t* __restrict__ lptr, int32_t* __restrict__ bcur,
+                  int2* __restrict__ stage, int32_t* __restrict__ lel) {
+    __shared__ int32_t hist[kB4MaxBuckets];
+    __shared__ int32_t base[kB4MaxBuckets];
+    const int nb = ((n_nodes - 1) >> shift) + 1;
+    constexpr int CH = kP4Block * kB4Items;
+    const int64_t e0 = (int64_t)blockIdx.x * CH;
+    for (int b = threadIdx.x; b < nb; b += kP4Block) hist[b] = 0;
+    __syncthreads();
+    int32_t lv[kB4Items], rk[kB4Items];
+    uint32_t key[kB4Items];
+#pragma unroll
+    for (int k = 0; k < kB4Items; ++k) {
+        const int64_t e = e0 + k * kP4Block + threadIdx.x;
+        lv[k] = -1;
+        if (e < n_entries) {
+            const int32_t v = __ldg(elems + e);
+            if ((uint32_t)v < (uint32_t)n_nodes) lv[k] = __ldg(lab + v);
+            lel[e] = lv[k];
+            if (lv[k] >= 0) {
+                const int32_t t = (int32_t)(e / nv);
+                key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
+                rk[k] = atomicAdd(&hist[lv[k] >> shift], 1);
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += kP4Block)
+        if (hist[b]) base[b] = __ldg(lptr + min((int64_t)b << shift, (int64_t)n_nodes)) + atomicAdd(bcur + b, hist[b]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kB4Items; ++k)
+        if (lv[k] >= 0) stage[base[lv[k] >> shift] + rk[k]] = make_int2(lv[k], (int32_t)key[k]);
+}
+
+// staged incidences in bucket order -> their label segments (total = lptr[N])
+__global__ void __launch_bounds__(kP4Block)
+k4_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage, int32_t* __restrict__ cursor,
+          uint32_t* __restrict__ linc) {
+    const int64_t n_staged = *total;
+    for (int64_t q0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; q0 < n_staged;
+         q0 += (int64_t)gridDim.x * blockDim.x * 4) {
+        int2 sv[4];
+        int32_t pos[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sv[u] = q0 + u < n_staged ? __ldg(stage + q0 + u) : make_int2(-1, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pos[u] = sv[u].x >= 0 ? atomicAdd(cursor + sv[u].x, 1) : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (sv[u].x >= 0) linc[pos[u]] = (uint32_t)sv[u].y;
     }
 }
 
@@ -248,19 +424,38 @@ struct V4 {
 template <int D, int L, int K, bool LIFT>
 struct V4Smem {  // one per column group
     using C = V4<D, L, K>;
+    static constexpr int NV = D + 1;
     alignas(16) int32_t row[C::HS];    // slot -> row (node id, -1 empty)
     alignas(16) int32_t crow[C::HS];   // occupied rows, compacted (-1 padded)
     int32_t cslot[C::HS];              // their slots
     int32_t frk[C::HS];                // slot -> free rank of the row (-1: Dirichlet)
-    uint32_t msk[C::HS][D + 1];        // slot -> pass-i mask over incidences
-    int32_t srow[C::HS];               // rows in ascending order
-    int32_t sfrk[C::HS];
-    double sval[C::HS];
-    double stv[LIFT ? C::HS : 1];      // lift: A(c, row), then A(c, row) u0[row]
-    alignas(16) double lb[C::LK];      // load shares in incidence order
-    alignas(16) double ld[C::LK];      // s_jj in incidence order
-    double itm[D + 1][C::LK];          // item (i, incidence) = s_ij of the incidence's element
-    uint32_t skey[C::LK];              // sorted incidence keys
+    uint32_t msk[C::HS][NV];           // slot -> pass-i mask over incidences
+    // items and folds first; once every fold is done the same bytes hold the
+    // column's ranked output (rows, free ranks, values, lift products)
+    union {
+        struct {
+            double itm[NV][C::LK];     // item (i, incidence) = s_ij of the incidence's element
+            double lb[C::LK];          // load shares in incidence order
+            double ld[C::LK];          // s_jj in incidence order
+        } in;
+        struct {
+            int32_t srow[C::MAXS];     // rows in ascending order
+            int32_t sfrk[C::MAXS];
+            double sval[C::MAXS];
+            double stv[C::MAXS];       // lift: A(c, row), then A(c, row) u0[row]
+        } out;
+    } u;
+    static_assert(sizeof(u.out) <= sizeof(u.in), "output must fit in the item space");
+};
+
+// The column groups of a warp access the same offsets of their own V4Smem at the
+// same time: a struct size that is a multiple of 128 B maps them all onto the same
+// banks (4-way conflicts in 3-D).  Pad so consecutive groups start 8 banks apart.
+template <class S>
+struct alignas(16) Padded {
+    static constexpr size_t kPad = (sizeof(S) % 128 == 32) ? 0 : ((160 - sizeof(S) % 128) % 128);
+    S s;
+    char pad[kPad == 0 ? 16 : kPad];
 };
 
 __device__ __forceinline__ double4 ld_xl(const double4* p) {
@@ -357,17 +552,20 @@ __device__ __forceinline__ double load_share(const ElemCol<2>& ec, int j, int32_
 //   after the stable passes sparse.hpp:79-89); exact zeros dropped
 //   (sparse.hpp:105); rows ranked by node id; A(free,free) keeps rows with a
 //   free rank.
-template <int D, int L, int K, bool LIFT>
-__global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_columns4(ColParams p) {
+template <int D, int L, int K, bool LIFT, int MINB>
+__global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColParams p) {
     using C = V4<D, L, K>;
     constexpr int NV = D + 1;
     constexpr int LK = C::LK;
-    __shared__ V4Smem<D, L, K, LIFT> sm_all[C::WARPS * C::GPW];
+    __shared__ Padded<V4Smem<D, L, K, LIFT>> sm_all[C::WARPS * C::GPW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gi = lane / L, g = lane % L;
     const unsigned gmask = (L == 32) ? kFull : (((1u << L) - 1) << (gi * L));
     const unsigned lower = (1u << lane) - 1;
-    V4Smem<D, L, K, LIFT>& sm = sm_all[warp * C::GPW + gi];
+    V4Smem<D, L, K, LIFT>& sm = sm_all[warp * C::GPW + gi].s;
+    static_assert(sizeof(Padded<V4Smem<D, L, K, LIFT>>) % 128 == 32 ||
+                      sizeof(Padded<V4Smem<D, L, K, LIFT>>) % 128 == 48,
+                  "group stride must be 8 (+-) banks off a multiple of 32");
     const Recip R3 = recip(3.0);
     const Recip R6 = recip(6.0);
 
@@ -377,7 +575,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= p.n_tiles) break;
         const int64_t sbase = tile * p.tile_cap;
-        int run_a = 0, run_f = 0;  // warp-uniform: entries staged so far in this tile
+        int run_a = 0;  // warp-uniform: entries staged so far in this tile
         bool bad = false;
         const int32_t lc0 = (int32_t)(tile * C::WTC);
         const int ncol_t = (int)min((int64_t)C::WTC, (int64_t)p.n_cols - lc0);
@@ -448,8 +646,6 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                     }
                 }
             }
-#pragma unroll
-            for (int kk = 0; kk < K; ++kk) sm.skey[kk * L + g] = key[kk];
             if (p.want_a) {
                 for (int h = g; h < C::HS; h += L) {
                     sm.row[h] = -1;
@@ -461,32 +657,51 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
             __syncwarp();
             // ---- 2. per incidence: geometry of column j of element t from the
             //      label-ordered nodes, staged; its off-diagonal items' rows inserted
+            // the element's vertex labels one incidence ahead: incidence kk+1's
+            // load is in flight while incidence kk is processed
+            auto key_at = [&](int kk) -> uint32_t {  // register select, no local memory
+                uint32_t k0 = key[0];
+#pragma unroll
+                for (int q2 = 1; q2 < K; ++q2) k0 = (kk == q2) ? key[q2] : k0;
+                return k0;
+            };
+            auto lel_of = [&](int kk) {
+                int4 v = make_int4(0, 0, 0, 0);
+                if (kk * L + g < m) {
+                    const int32_t tt = (int32_t)(key_at(kk) & 0x3FFFFFFFu);
+                    if constexpr (D == 3) {
+                        v = __ldg(reinterpret_cast<const int4*>(p.lel) + tt);
+                    } else {
+                        v.x = __ldg(p.lel + (size_t)tt * NV);
+                        v.y = __ldg(p.lel + (size_t)tt * NV + 1);
+                        v.z = __ldg(p.lel + (size_t)tt * NV + 2);
+                    }
+                }
+                return v;
+            };
+            int4 lel_next = lel_of(0);
 #pragma unroll 1
             for (int kk = 0; kk < K; ++kk) {
                 const int e = kk * L + g;
+                const int4 lel_cur = lel_next;
+                if (kk + 1 < K) lel_next = lel_of(kk + 1);
                 if (e >= m) {
                     if (e < LK) {
 #pragma unroll
-                        for (int i = 0; i < NV; ++i) sm.itm[i][e] = 0.0;
-                        sm.lb[e] = 0.0;
-                        sm.ld[e] = 0.0;
+                        for (int i = 0; i < NV; ++i) sm.u.in.itm[i][e] = 0.0;
+                        sm.u.in.lb[e] = 0.0;
+                        sm.u.in.ld[e] = 0.0;
                     }
                     continue;
                 }
-                const uint32_t ky = sm.skey[e];
+                const uint32_t ky = key_at(kk);
                 const int32_t t_ = (int32_t)(ky & 0x3FFFFFFFu);
                 const int j_ = (int)(ky >> 30);
                 int32_t lv[NV];
-                if constexpr (D == 3) {
-                    const int4 ev = __ldg(reinterpret_cast<const int4*>(p.lel) + t_);
-                    lv[0] = ev.x;
-                    lv[1] = ev.y;
-                    lv[2] = ev.z;
-                    lv[3] = ev.w;
-                } else {
-#pragma unroll
-                    for (int i = 0; i < NV; ++i) lv[i] = __ldg(p.lel + (size_t)t_ * NV + i);
-                }
+                lv[0] = lel_cur.x;
+                lv[1] = lel_cur.y;
+                lv[2] = lel_cur.z;
+                if constexpr (D == 3) lv[3] = lel_cur.w;
                 bool okv = true;
 #pragma unroll
                 for (int i = 0; i < NV; ++i) okv = okv && lv[i] >= 0;
@@ -521,19 +736,23 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                 double sjj = 0.0;
 #pragma unroll
                 for (int i = 0; i < NV; ++i) {
-                    sm.itm[i][e] = s[i];
+                    sm.u.in.itm[i][e] = s[i];
                     if (i == j_) sjj = s[i];
                 }
-                sm.lb[e] = lsh;
-                sm.ld[e] = sjj;
+                sm.u.in.lb[e] = lsh;
+                sm.u.in.ld[e] = sjj;
                 if (!p.want_a) continue;
+                // exact-zero items are skipped: x + (+-0) == x for x != 0, a zero
+                // prefix only changes the sign of a zero the next nonzero item
+                // absorbs, and an all-zero entry is dropped anyway (sparse.hpp:105)
+                uint32_t todo = 0;
 #pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    // exact-zero items are skipped: x + (+-0) == x for x != 0, a zero
-                    // prefix only changes the sign of a zero the next nonzero item
-                    // absorbs, and an all-zero entry is dropped anyway (sparse.hpp:105)
-                    if (i == j_ || s[i] == 0.0) continue;
-                    const int32_t r = R[i];
+                for (int i = 0; i < NV; ++i) todo |= (i != j_ && s[i] != 0.0) ? (1u << i) : 0u;
+#pragma unroll 1
+                for (; todo; todo &= todo - 1) {
+                    const int i = __ffs(todo) - 1;
+                    const int32_t r = i == 0 ? R[0] : i == 1 ? R[1] : (i == 2 || D == 2) ? R[2] : R[D];
+                    const int32_t fr = i == 0 ? FR[0] : i == 1 ? FR[1] : (i == 2 || D == 2) ? FR[2] : FR[D];
                     uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - lg2c(C::HS));
                     int slot = -1;
 #pragma unroll 1
@@ -546,7 +765,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                         h = (h + 1) & (C::HS - 1);
                     }
                     if (slot >= 0) {
-                        sm.frk[slot] = FR[i];
+                        sm.frk[slot] = fr;
                         atomicOr(&sm.msk[slot][i], 1u << e);
                     } else {
                         bad = true;
@@ -557,7 +776,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
             // ---- 3. b and the diagonal: sequential folds in incidence order (lanes 0 / 1)
             double fold = g == 0 ? 0.0 : -0.0;
             if (g < 2) {
-                const double* src = g == 0 ? sm.lb : sm.ld;
+                const double* src = g == 0 ? sm.u.in.lb : sm.u.in.ld;
                 const double2* src2 = reinterpret_cast<const double2*>(src);
                 const int np = m >> 1;
 #pragma unroll 2
@@ -571,6 +790,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
             const double b = __shfl_sync(kFull, fold, 0, L);
             const double dg = __shfl_sync(kFull, fold, 1, L);
             double ylift = 0.0;
+            uint64_t meta = 0;  // staging: in-tile offset | count of A, then of A(free, free)
             if (p.want_a) {
                 // ---- 4. the diagonal slot, the folds, rows ranked, zero drop
                 if (g == 0 && act && m > 0) {
@@ -606,39 +826,64 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
 #pragma unroll
                     for (int kk = 0; kk < K; ++kk) {
                         const int e = kk * L + g;
-                        const int je = e < m ? (int)(sm.skey[e] >> 30) : -1;
+                        const int je = e < m ? (int)(key[kk] >> 30) : -1;
 #pragma unroll
                         for (int jj = 0; jj < NV; ++jj)
                             jm[jj] |= ((__ballot_sync(kFull, je == jj) & gmask) >> (gi * L)) << (kk * L);
                     }
                 }
-                // one lane per occupied slot (the compacted list)
-#pragma unroll 1
-                for (int k = g; k < nocc; k += L) {
-                    const int h = sm.cslot[k];
-                    const int32_t r = sm.crow[k];
-                    {
-                        double acc = dg;
-                        double tacc = dg;  // A(c, r): the transposed entry (lift only)
+                // one lane per occupied slot (the compacted list): every fold into
+                // registers first, then the ranked output over the item space
+                constexpr int NI = C::HS / L;
+                double accv[NI], taccv[NI];
+                int32_t rowv[NI], frkv[NI];
+#pragma unroll
+                for (int ii = 0; ii < NI; ++ii) {
+                    const int k = g + ii * L;
+                    rowv[ii] = -1;
+                    frkv[ii] = -1;
+                    accv[ii] = dg;
+                    taccv[ii] = dg;  // A(c, r): the transposed entry (lift only)
+                    if (k < nocc) {
+                        const int h = sm.cslot[k];
+                        const int32_t r = sm.crow[k];
+                        rowv[ii] = r;
+                        frkv[ii] = sm.frk[h];
                         if (r != c) {
-                            acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
+                            double acc = -0.0;  // -0.0 + x == x: the fold starts at its first value
 #pragma unroll
                             for (int i = 0; i < NV; ++i)
                                 for (uint32_t mm = sm.msk[h][i]; mm; mm &= mm - 1)
-                                    acc = acc + sm.itm[i][__ffs(mm) - 1];
+                                    acc = acc + sm.u.in.itm[i][__ffs(mm) - 1];
+                            accv[ii] = acc;
                             if constexpr (LIFT) {
                                 // A(c, r) folds the same items in (i_c*(d+1)+j_r, t) order:
                                 // the incidence's own j first (incidences are sorted by j:
                                 // contiguous ranges jm[jj]), then the pass, then incidences
-                                tacc = -0.0;
+                                double tacc = -0.0;
 #pragma unroll
                                 for (int jj = 0; jj < NV; ++jj)
 #pragma unroll
                                     for (int i = 0; i < NV; ++i)
                                         for (uint32_t mm = sm.msk[h][i] & jm[jj]; mm; mm &= mm - 1)
-                                            tacc = tacc + sm.itm[i][__ffs(mm) - 1];
+                                            tacc = tacc + sm.u.in.itm[i][__ffs(mm) - 1];
+                                taccv[ii] = tacc;
                             }
                         }
+                    }
+                }
+                if constexpr (!LIFT) {
+                    // ranked output straight from registers: bit rk of `kept` = the row
+                    // of rank rk survives the zero drop (sparse.hpp:105); its place in
+                    // the column is the number of kept rows ranked below it
+                    const bool col_free = fc_c >= 0 && p.want_sys;
+                    int rkv[NI];
+                    uint32_t kept = 0, keptf = 0;
+#pragma unroll
+                    for (int ii = 0; ii < NI; ++ii) {
+                        rkv[ii] = -1;
+                        const int32_t r = rowv[ii];
+                        if (r < 0) continue;
                         int rk = 0;  // rows below r; unused entries (-1) compare as huge
                         const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
                         for (int qq = 0; qq < n4; ++qq) {
@@ -646,12 +891,58 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                             rk += ((uint32_t)v.x < (uint32_t)r) + ((uint32_t)v.y < (uint32_t)r) +
                                   ((uint32_t)v.z < (uint32_t)r) + ((uint32_t)v.w < (uint32_t)r);
                         }
-                        if (rk < C::MAXS) {
-                            sm.srow[rk] = r;
-                            sm.sfrk[rk] = sm.frk[h];
-                            sm.sval[rk] = acc;
-                            if constexpr (LIFT) sm.stv[rk] = tacc;
+                        rkv[ii] = rk;
+                        if (rk < C::MAXS && accv[ii] != 0.0) {
+                            kept |= 1u << rk;
+                            if (col_free && frkv[ii] >= 0) keptf |= 1u << rk;
                         }
+                    }
+#pragma unroll
+                    for (int o = 1; o < L; o <<= 1) {
+                        kept |= __shfl_xor_sync(kFull, kept, o, L);
+                        keptf |= __shfl_xor_sync(kFull, keptf, o, L);
+                    }
+                    if (nocc > C::MAXS) {
+                        bad = true;
+                        kept = keptf = 0;
+                    }
+                    const int na = __popc(kept), nf = __popc(keptf);
+                    int pa = na;  // inclusive prefix over the groups (column order)
+#pragma unroll
+                    for (int o = L; o < 32; o <<= 1) {
+                        const int ya = __shfl_up_sync(kFull, pa, o);
+                        if (lane >= o) pa += ya;
+                    }
+                    const int tot_a = __shfl_sync(kFull, pa, 31);
+                    const int wa = run_a + pa - na;  // this column's first slot
+                    meta = (uint64_t)wa | ((uint64_t)na << 16) | ((uint64_t)nf << 24);
+#pragma unroll
+                    for (int ii = 0; ii < NI; ++ii) {
+                        const int rk = rkv[ii];
+                        if (rk < 0 || !((kept >> rk) & 1u)) continue;
+                        const int64_t o = sbase + wa + __popc(kept & ((1u << rk) - 1));
+                        reinterpret_cast<int2*>(p.st_a_row)[o] = make_int2(rowv[ii], p.want_sys ? frkv[ii] : -1);
+                        p.st_a_val[o] = accv[ii];
+                    }
+                    run_a += tot_a;
+                } else {
+                __syncwarp();
+#pragma unroll
+                for (int ii = 0; ii < NI; ++ii) {
+                    const int32_t r = rowv[ii];
+                    if (r < 0) continue;
+                    int rk = 0;  // rows below r; unused entries (-1) compare as huge
+                    const int4* r4 = reinterpret_cast<const int4*>(sm.crow);
+                    for (int qq = 0; qq < n4; ++qq) {
+                        const int4 v = r4[qq];
+                        rk += ((uint32_t)v.x < (uint32_t)r) + ((uint32_t)v.y < (uint32_t)r) +
+                              ((uint32_t)v.z < (uint32_t)r) + ((uint32_t)v.w < (uint32_t)r);
+                    }
+                    if (rk < C::MAXS) {
+                        sm.u.out.srow[rk] = r;
+                        sm.u.out.sfrk[rk] = frkv[ii];
+                        sm.u.out.sval[rk] = accv[ii];
+                        if constexpr (LIFT) sm.u.out.stv[rk] = taccv[ii];
                     }
                 }
                 if (nocc > C::MAXS) {
@@ -668,12 +959,12 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                         const int qq = base + g;
                         bool use = false;
                         if (qq < nslot) {
-                            const double a = sm.stv[qq];
-                            const int32_t r = sm.srow[qq];
-                            if (a != 0.0 && sm.sfrk[qq] < 0) {
+                            const double a = sm.u.out.stv[qq];
+                            const int32_t r = sm.u.out.srow[qq];
+                            if (a != 0.0 && sm.u.out.sfrk[qq] < 0) {
                                 const double u = node_field4(p.g_dir, p.nodes, D, r);
                                 use = u != 0.0;
-                                sm.stv[qq] = a * u;
+                                sm.u.out.stv[qq] = a * u;
                             }
                         }
                         umask |= ((__ballot_sync(kFull, use) & gmask) >> (gi * L)) << base;
@@ -681,68 +972,54 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                     __syncwarp();
                     if (g == 0) {
                         double yy = 0.0;
-                        for (uint32_t mm = umask; mm; mm &= mm - 1) yy = yy + sm.stv[__ffs(mm) - 1];
+                        for (uint32_t mm = umask; mm; mm &= mm - 1) yy = yy + sm.u.out.stv[__ffs(mm) - 1];
                         ylift = yy;
                     }
                     __syncwarp();
                 }
                 const bool col_free = fc_c >= 0;
-                // compaction in chunks of L entries: counts per group first (the
-                // groups of a warp stage their columns one after another)
+                // compaction in chunks of L entries into ONE staged run per column:
+                // {row, free rank of the row or -1} + value; A(free, free) is the
+                // subset with a free rank in a free column (placed by k4_place)
                 constexpr int NCH = (C::MAXS + L - 1) / L;
                 int na = 0, nf = 0;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     const int qq = ch * L + g;
                     const bool in = qq < nslot;
-                    const double v = in ? sm.sval[qq] : 0.0;
+                    const double v = in ? sm.u.out.sval[qq] : 0.0;
                     const bool keep = in && v != 0.0;  // sparse.hpp:105
-                    const bool keepf = keep && col_free && p.want_sys && sm.sfrk[qq] >= 0;
+                    const bool keepf = keep && col_free && p.want_sys && sm.u.out.sfrk[qq] >= 0;
                     na += __popc(__ballot_sync(kFull, keep) & gmask);
                     nf += __popc(__ballot_sync(kFull, keepf) & gmask);
                 }
-                int pa = na, pf = nf;  // inclusive prefix over the groups (column order)
+                int pa = na;  // inclusive prefix over the groups (column order)
 #pragma unroll
                 for (int o = L; o < 32; o <<= 1) {
                     const int ya = __shfl_up_sync(kFull, pa, o);
-                    const int yf = __shfl_up_sync(kFull, pf, o);
-                    if (lane >= o) {
-                        pa += ya;
-                        pf += yf;
-                    }
+                    if (lane >= o) pa += ya;
                 }
-                const int tot_a = __shfl_sync(kFull, pa, 31), tot_f = __shfl_sync(kFull, pf, 31);
-                int wa = run_a + pa - na, wf = run_f + pf - nf;  // this column's first slot
-                if (act && g == 0) {
-                    p.colcnt_a[l] = wa + na;
-                    if (p.want_sys) p.colcnt_f[l] = wf + nf;
-                }
+                const int tot_a = __shfl_sync(kFull, pa, 31);
+                int wa = run_a + pa - na;  // this column's first slot
+                meta = (uint64_t)wa | ((uint64_t)na << 16) | ((uint64_t)nf << 24);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     const int qq = ch * L + g;
                     const bool in = qq < nslot;
-                    const double v = in ? sm.sval[qq] : 0.0;
-                    const int32_t r = in ? sm.srow[qq] : 0;
-                    const int32_t fr = in ? sm.sfrk[qq] : -1;
+                    const double v = in ? sm.u.out.sval[qq] : 0.0;
+                    const int32_t r = in ? sm.u.out.srow[qq] : 0;
+                    const int32_t fr = (in && p.want_sys) ? sm.u.out.sfrk[qq] : -1;
                     const bool keep = in && v != 0.0;
-                    const bool keepf = keep && col_free && p.want_sys && fr >= 0;
                     const unsigned ba = __ballot_sync(kFull, keep) & gmask;
-                    const unsigned bf = __ballot_sync(kFull, keepf) & gmask;
                     if (keep) {
                         const int64_t o = sbase + wa + __popc(ba & lower);
-                        p.st_a_row[o] = r;
+                        reinterpret_cast<int2*>(p.st_a_row)[o] = make_int2(r, fr);
                         p.st_a_val[o] = v;
                     }
-                    if (keepf) {
-                        const int64_t o = sbase + wf + __popc(bf & lower);
-                        p.st_f_row[o] = fr;
-                        p.st_f_val[o] = v;
-                    }
                     wa += __popc(ba);
-                    wf += __popc(bf);
                 }
                 run_a += tot_a;
-                run_f += tot_f;
+                }  // LIFT
             }
             // ---- per-column vectors, by label: {b, u0, b - A u0}
             if (act && g == 0) {
@@ -751,7 +1028,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
                     u0 = fc_c < 0 ? node_field4(p.g_dir, p.nodes, D, c) : 0.0;
                     bmod = LIFT ? b - ylift : b - 0.0;  // system.hpp:197-198
                 }
-                p.vst[l] = make_double4(b, u0, bmod, 0.0);
+                p.vst[l] = make_double4(b, u0, bmod, __longlong_as_double((long long)meta));
             }
             __syncwarp();
         }
@@ -760,98 +1037,118 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, D == 3 ? 8 : 4) k_col
 }
 
 // ===========================================================================
-// placement: label-ordered staging -> node-id-ordered CSC and vectors
+// placement: label-ordered staging -> node-id-ordered CSC and vectors, one pass
 // ===========================================================================
-// entries of label l: tile l / wtc, in-tile inclusive count colcnt[l]
-__device__ __forceinline__ int32_t col_count(const int32_t* colcnt, int32_t l, int wtc) {
-    return colcnt[l] - ((l % wtc) ? colcnt[l - 1] : 0);
-}
+// Tile = 256 consecutive node ids (one per thread), tiles taken in order from a
+// ticket.  Each node's label record vst[lab[v]] holds its vectors and, packed in
+// .w, the in-tile staging offset and count of its A and A(free, free) entries
+// (meta of k_columns4).  The column pointers are an exclusive scan over node ids
+// (block scan + decoupled look-back on (nnz_A, nnz_Aff) packed in 64 bits); a
+// warp's 32 consecutive columns are one contiguous destination run, copied with
+// every store instruction writing 32 consecutive entries.
+constexpr int kPlaceThreads = 256;
 
-// Warp per 32 consecutive nodes.  Their destination runs are contiguous in the
-// CSC arrays, so lanes copy entry q of the warp's run (found by a binary search
-// over the 32 column prefixes): every store instruction writes 32 consecutive
-// entries; the loads gather a few staged runs.
-__global__ void __launch_bounds__(256) k4_place(ColParams p, int wtc, const int32_t* __restrict__ lab,
-                                                const int32_t* __restrict__ ffscan) {
+__global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, int wtc, const int32_t* __restrict__ lab,
+                                                          uint64_t* __restrict__ status,
+                                                          unsigned int* __restrict__ ticket) {
+    __shared__ int64_t warp_sums[kPlaceThreads / 32];
+    __shared__ int64_t s_tile, s_excl;
     const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int32_t N = p.n_cols;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w * 32 < N; w += nwarps) {
-        const int32_t v = (int32_t)(w * 32) + lane;
-        const bool in = v < N;
-        const int32_t l = in ? __ldg(lab + v) : 0;
-        const int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + v) : -1;
-        // vectors
-        if (in) {
-            const double4 vs = p.vst[l];
-            if (p.want_b) p.b[v] = vs.x;
-            if (p.want_sys) {
-                p.u0[v] = vs.y;
-                p.b_mod[v] = vs.z;
-                if (fr >= 0) {
-                    p.b_f[fr] = vs.z;
-                    p.ff_col_ptr[fr] = __ldg(ffscan + v);
-                }
-            }
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int32_t v = (int32_t)(tile * kPlaceThreads) + threadIdx.x;
+    const bool in = v < N;
+    const int32_t l = in ? __ldg(lab + v) : 0;
+    const int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + v) : -1;
+    double4 vs = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (in) vs = ld_xl(p.vst + l);
+    const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
+    const int32_t ca = in ? (int32_t)((meta >> 16) & 0xFF) : 0;
+    const int32_t cf = fr >= 0 ? (int32_t)((meta >> 24) & 0xFF) : 0;
+    const int64_t src = (int64_t)(l / wtc) * p.tile_cap + (int64_t)(meta & 0xFFFF);
+    if (in) {
+        if (p.want_b) p.b[v] = vs.x;
+        if (p.want_sys) {
+            p.u0[v] = vs.y;
+            p.b_mod[v] = vs.z;
+            if (fr >= 0) p.b_f[fr] = vs.z;
         }
-        // A(free, free) col_ptr[n_free] = its nnz (free_rank[N] = n_free, k_partition's scan)
-        if (w == 0 && lane == 0 && p.want_sys && p.want_a)
-            p.ff_col_ptr[__ldg(p.fidx + 2 * (int64_t)N + 1)] = __ldg(ffscan + N);
-        if (!p.want_a) continue;
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {  // 0: A, 1: A(free, free)
-            if (f == 1 && !p.want_sys) break;
-            const int32_t* colcnt = f ? p.colcnt_f : p.colcnt_a;
-            const int32_t* srow = f ? p.st_f_row : p.st_a_row;
-            const double* sval = f ? p.st_f_val : p.st_a_val;
-            int32_t* drow = f ? p.ff_row_idx : p.row_idx;
-            double* dval = f ? p.ff_values : p.values;
-            const int64_t cap = f ? p.cap_ff : p.cap_a;
-            const bool has = in && (f == 0 || fr >= 0);
-            const int32_t len = has ? col_count(colcnt, l, wtc) : 0;
-            const int64_t src = has ? (int64_t)(l / wtc) * p.tile_cap + colcnt[l] - len : 0;
-            int32_t pre = len;  // inclusive prefix over lanes
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(kFull, pre, o);
-                if (lane >= o) pre += y;
-            }
-            const int32_t total = __shfl_sync(kFull, pre, 31);
-            if (total == 0) continue;
-            const int32_t excl = pre - len;
-            // first destination: col_ptr of the warp's first column (f = 0), or of its
-            // first free column (f = 1)
-            int32_t d0;
-            if (f == 0) {
-                d0 = p.col_ptr[w * 32];
-            } else {
-                const unsigned fb = __ballot_sync(kFull, has);
-                const int first = __ffs(fb) - 1;
-                d0 = __shfl_sync(kFull, in ? __ldg(ffscan + v) : 0, first);
-            }
-            if ((int64_t)d0 + total > cap) {
-                if (lane == 0) atomicOr(p.err, DERR_CAPACITY);
-                continue;
-            }
-            for (int32_t q0 = 0; q0 < total; q0 += 32) {
-                const int32_t qq = q0 + lane;
-                // largest k with excl[k] <= qq (columns with len 0 share prefixes:
-                // the search lands on the last of them, whose run holds qq)
-                int k = 0;
-#pragma unroll
-                for (int stp = 16; stp > 0; stp >>= 1) {
-                    const int32_t ek = __shfl_sync(kFull, excl, k + stp);
-                    if (ek <= qq) k += stp;
-                }
-                const int32_t ek = __shfl_sync(kFull, excl, k);
-                const int64_t sk = __shfl_sync(kFull, src, k);
-                if (qq < total) {
-                    const int64_t s = sk + (qq - ek);
-                    drow[d0 + qq] = __ldcs(srow + s);
-                    dval[d0 + qq] = __ldcs(sval + s);
-                }
-            }
+    }
+    if (!p.want_a) return;
+    // exclusive prefix over node ids of (A count, A(free, free) count)
+    int64_t total;
+    int64_t excl = block_exclusive_sum<kPlaceThreads>((int64_t)ca | ((int64_t)cf << 32), warp_sums, total);
+    if (threadIdx.x < 32) {
+        const uint64_t e = warp_lookback(status, tile, (uint64_t)total);
+        if (threadIdx.x == 0) s_excl = (int64_t)e;
+    }
+    __syncthreads();
+    excl += s_excl;
+    const int32_t pa = (int32_t)(excl & 0xFFFFFFFF), pf = (int32_t)(excl >> 32);
+    if (in) {
+        p.col_ptr[v] = pa;
+        if (fr >= 0) p.ff_col_ptr[fr] = pf;
+        if (v == N - 1) {
+            p.col_ptr[N] = pa + ca;
+            if (p.want_sys) p.ff_col_ptr[__ldg(p.fidx + 2 * (int64_t)N + 1)] = pf + cf;
         }
+        if ((int64_t)pa + ca > p.cap_a || (p.want_sys && (int64_t)pf + cf > p.cap_ff)) atomicOr(p.err, DERR_CAPACITY);
+    }
+    // the warp's 32 columns are one contiguous run of A: every store writes 32
+    // consecutive entries; A(free, free) takes the entries with a free row in a
+    // free column, at the column's pointer + their rank among them
+    int32_t pre = ca;  // inclusive prefix over the warp's lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, pre, o);
+        if (lane >= o) pre += y;
+    }
+    const int32_t total_w = __shfl_sync(kFull, pre, 31);
+    if (total_w == 0) return;
+    const int32_t ex = pre - ca;
+    const int32_t d0 = __shfl_sync(kFull, pa, 0);
+    if ((int64_t)d0 + total_w > p.cap_a) return;  // flagged above
+    const int2* srf = reinterpret_cast<const int2*>(p.st_a_row);
+    const int cfree_l = fr >= 0 ? 1 : 0;
+    int carry_k = -1, carry = 0;
+    for (int32_t q0 = 0; q0 < total_w; q0 += 32) {
+        const int32_t qq = q0 + lane;
+        // largest k with ex[k] <= qq (lanes with len 0 share prefixes: the search
+        // lands on the last of them, whose run holds qq)
+        int k = 0;
+#pragma unroll
+        for (int stp = 16; stp > 0; stp >>= 1) {
+            const int32_t ek = __shfl_sync(kFull, ex, k + stp);
+            if (ek <= qq) k += stp;
+        }
+        const int32_t ek = __shfl_sync(kFull, ex, k);
+        const int64_t sk = __shfl_sync(kFull, src, k);
+        const int32_t pfk = __shfl_sync(kFull, pf, k);
+        const int cfree = __shfl_sync(kFull, cfree_l, k);
+        int2 rf = make_int2(0, -1);
+        double val = 0.0;
+        if (qq < total_w) {
+            const int64_t s = sk + (qq - ek);
+            rf = __ldcs(srf + s);
+            val = __ldcs(p.st_a_val + s);
+            p.row_idx[d0 + qq] = rf.x;
+            p.values[d0 + qq] = val;
+        }
+        const bool isf = qq < total_w && p.want_sys && cfree && rf.y >= 0;
+        const unsigned bal = __ballot_sync(kFull, isf);
+        const int start = ek > q0 ? (int)(ek - q0) : 0;  // column k's first lane in this round
+        const unsigned below = (1u << lane) - 1, before = (1u << start) - 1;
+        const int rank = __popc(bal & below & ~before) + (k == carry_k ? carry : 0);
+        if (isf) {
+            p.ff_row_idx[pfk + rank] = rf.y;
+            p.ff_values[pfk + rank] = val;
+        }
+        // the column holding lane 31 may continue into the next round
+        const int k31 = __shfl_sync(kFull, k, 31), st31 = __shfl_sync(kFull, start, 31);
+        carry = (k31 == carry_k ? carry : 0) + __popc(bal & ~((1u << st31) - 1));
+        carry_k = k31;
     }
 }
 
@@ -880,15 +1177,47 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     int32_t* ilab = lp.ilab.as<int32_t>();
     FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
     FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
-    if (n_entries > 0) {
-        const int64_t blocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
-        k4_count<<<(int)blocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, lab, ilab,
-                                                  misc);
+    const int64_t cblocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
+    const char* lenv = std::getenv("FL_LABELS");
+    if (lenv && lenv[0] == 'f') {
+        // first touch in element order (no coordinates involved)
+        if (n_entries > 0) {
+            k4_count<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, lab, ilab, misc);
+            count_launch(ctx);
+        }
+        if (N > 0) {
+            k4_untouched<<<div_up(N, kP4Block), kP4Block, 0, s>>>(N, cnt, lab, ilab, misc);
+            count_launch(ctx);
+        }
+    } else if (N > 0) {
+        // Morton cells of ~64 nodes: 2^(dim*bits) cells
+        const int dim = mesh->dim;
+        int bits = 1;
+        while (bits < (dim == 3 ? 10 : 15) && ((int64_t)1 << (dim * (bits + 1))) * 64 <= (int64_t)N) ++bits;
+        const int64_t ncell = (int64_t)1 << (dim * bits);
+        const int nparts = std::min(div_up(N, 256), ctx->sm_count * 4);
+        FL_TRY(lp.cells.ensure(sizeof(int32_t) * ((size_t)N + 2 * (size_t)ncell + 2) + sizeof(double) * (6 * (size_t)nparts + 1)));
+        int32_t* cellv = lp.cells.as<int32_t>();
+        int32_t* ccnt = cellv + N;
+        int32_t* coff = ccnt + ncell + 1;
+        double* part = reinterpret_cast<double*>(coff + ncell + 1 + ((N + 2 * ncell + 2) & 1));
+        FL_CUDA(cudaMemsetAsync(ccnt, 0, sizeof(int32_t) * (size_t)(ncell + 1), s));
+        k4_bbox<<<nparts, 256, 0, s>>>(N, dim, mesh->nodes.as<double>(), part);
         count_launch(ctx);
-    }
-    if (N > 0) {
-        k4_untouched<<<div_up(N, kP4Block), kP4Block, 0, s>>>(N, cnt, lab, ilab, misc);
+        k4_cell<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, dim, bits, nparts, mesh->nodes.as<double>(),
+                                                                          part, cellv, ccnt);
         count_launch(ctx);
+        FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(std::max<int64_t>(N, ncell))));
+        const int32_t* cc = ccnt;
+        FL_CUDA(launch_scan<int32_t>(ncell, [cc] __device__(int64_t i) { return (int64_t)cc[i]; }, coff,
+                                     ctx->scan_ws.p, s));
+        count_launch(ctx);
+        k4_cell_scatter<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, cellv, coff, lab, ilab);
+        count_launch(ctx);
+        if (n_entries > 0) {
+            k4_count_plain<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, misc);
+            count_launch(ctx);
+        }
     }
     const int32_t* cc = cnt;
     const int32_t* il = ilab;
@@ -898,7 +1227,27 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     count_launch(ctx);
     // fill cursors start at the segment offsets
     FL_CUDA(cudaMemcpyAsync(cnt, lp.lptr.p, sizeof(int32_t) * ((size_t)N + 1), cudaMemcpyDeviceToDevice, s));
-    if (n_entries > 0) {
+    // bucketed fill for large 2-D meshes (FL_PLAN=0|1 overrides; the element order
+    // of a 3-D mesh is left spatial by every generator here, C5 included)
+    const char* penv = std::getenv("FL_PLAN");
+    const bool bucketed = n_entries > 0 &&
+                          (penv ? penv[0] == '1' : (mesh->dim == 2 && n_entries >= ((int64_t)1 << 26)));
+    if (bucketed) {
+        int shift = 0;
+        while (((int64_t)(N - 1) >> shift) + 1 > kB4MaxBuckets) ++shift;
+        const int nb = ((N - 1) >> shift) + 1;
+        FL_TRY(lp.stage.ensure(sizeof(int2) * (size_t)n_entries + sizeof(int32_t) * (kB4MaxBuckets + 1)));
+        int2* stg = lp.stage.as<int2>();
+        int32_t* bcur = reinterpret_cast<int32_t*>(stg + n_entries);
+        FL_CUDA(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (size_t)(nb + 1), s));
+        const int64_t chunks = (n_entries + kP4Block * kB4Items - 1) / (kP4Block * kB4Items);
+        k4_bucket_scatter<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, shift, mesh->elems.as<int32_t>(), lab,
+                                                           lp.lptr.as<int32_t>(), bcur, stg, lp.lel.as<int32_t>());
+        count_launch(ctx);
+        const int bgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, kP4Block * 4), 1), INT_MAX);
+        k4_fill_b<<<bgrid, kP4Block, 0, s>>>(lp.lptr.as<int32_t>() + N, stg, cnt, lp.linc.as<uint32_t>());
+        count_launch(ctx);
+    } else if (n_entries > 0) {
         constexpr int U = 4;
         const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
         k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, mesh->elems.as<int32_t>(), lab, cnt,
@@ -931,22 +1280,32 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     return FL_OK;
 }
 
-template <int D, int L, int K, bool LIFT>
+template <int D, int L, int K, bool LIFT, int MINB>
 static int launch4(fl_ctx* ctx, ColParams& p) {
     using C = V4<D, L, K>;
+    auto kern = k_columns4<D, L, K, LIFT, MINB>;
     int per_sm = 1;
-    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_columns4<D, L, K, LIFT>, C::WARPS * 32, 0));
+    FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WARPS * 32, 0));
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>((p.n_tiles + C::WARPS - 1) / C::WARPS, (int64_t)ctx->sm_count * std::max(per_sm, 1)));
-    k_columns4<D, L, K, LIFT><<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
+    kern<<<(int)grid, C::WARPS * 32, 0, ctx->stream>>>(p);
     count_launch(ctx);
     FL_CUDA(cudaGetLastError());
     return FL_OK;
 }
 
+// resident CTAs per SM the kernel is compiled for (registers); FL_V4_MINB=8|10
+// selects the 3-D variant (tuning experiments)
 template <int D, int L, int K>
 static int launch4_sel(fl_ctx* ctx, ColParams& p) {
-    return p.need_lift ? launch4<D, L, K, true>(ctx, p) : launch4<D, L, K, false>(ctx, p);
+    if constexpr (D == 3) {
+        const char* e = std::getenv("FL_V4_MINB");
+        if (e && e[0] == '8')
+            return p.need_lift ? launch4<D, L, K, true, 8>(ctx, p) : launch4<D, L, K, false, 8>(ctx, p);
+        return p.need_lift ? launch4<D, L, K, true, 10>(ctx, p) : launch4<D, L, K, false, 10>(ctx, p);
+    } else {
+        return p.need_lift ? launch4<D, L, K, true, 4>(ctx, p) : launch4<D, L, K, false, 4>(ctx, p);
+    }
 }
 
 // The column pass of fl_assemble on the label plan (whole mesh, no Neumann data:
@@ -961,7 +1320,6 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     const int maxs = dim == 2 ? V4<2, 8, 1>::MAXS : V4<3, 8, 4>::MAXS;
     FL_TRY(res->v4[0].ensure(sizeof(double4) * ((size_t)N + 1)));  // xl
     FL_TRY(res->v4[1].ensure(sizeof(double4) * ((size_t)N + 1)));  // vst
-    FL_TRY(res->v4[2].ensure(sizeof(int32_t) * ((size_t)N + 2)));  // A_ff column scan by node id
     double4* xl = res->v4[0].as<double4>();
     p.xl = xl;
     p.vst = res->v4[1].as<double4>();
@@ -975,6 +1333,9 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
         count_launch(ctx);
     }
     FL_TRY(prepare_staging(ctx, p, res, wtc, (int64_t)wtc * maxs));
+    // one staged run per column: int2 {row, free rank} + value (A(free, free) rides along)
+    FL_TRY(res->stage[0].ensure(sizeof(int2) * (size_t)p.n_tiles * (size_t)p.tile_cap));
+    p.st_a_row = res->stage[0].as<int32_t>();
     FL_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(uint32_t), s));
     if (ctx->profile) {
         FL_CUDA(cudaEventRecord(ctx->ev[5], s));
@@ -988,35 +1349,20 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
         if (kmax <= 8) FL_TRY((launch4_sel<2, 8, 1>(ctx, p)));
         else FL_TRY((launch4_sel<2, 8, 2>(ctx, p)));
     } else {
-        FL_TRY((launch4_sel<3, 8, 4>(ctx, p)));
+        // FL_V4_SHAPE=16x2: 16 lanes x 2 incidences, 2 columns per warp (experiment)
+        const char* sh = std::getenv("FL_V4_SHAPE");
+        if (sh && sh[0] == '1') FL_TRY((launch4_sel<3, 16, 2>(ctx, p)));
+        else FL_TRY((launch4_sel<3, 8, 4>(ctx, p)));
     }
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], s));
-    // placement: column pointers in node-id order, then the copy
-    const int32_t* labp = lp.lab.as<int32_t>();
-    int32_t* ffscan = res->v4[2].as<int32_t>();
-    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(N)));
-    if (p.want_a) {
-        const int32_t* ca = p.colcnt_a;
-        const int w = wtc;
-        FL_CUDA(launch_scan<int32_t>(
-            N, [ca, labp, w] __device__(int64_t v) { return (int64_t)col_count(ca, labp[v], w); }, p.col_ptr,
-            ctx->scan_ws.p, s));
-        count_launch(ctx);
-        if (p.want_sys) {
-            const int32_t* cf = p.colcnt_f;
-            const int32_t* fx = p.fidx;
-            FL_CUDA(launch_scan<int32_t>(
-                N,
-                [cf, labp, fx, w] __device__(int64_t v) {
-                    return (int64_t)(fx[v] >= 0 ? col_count(cf, labp[v], w) : 0);
-                },
-                ffscan, ctx->scan_ws.p, s));
-            count_launch(ctx);
-        }
-    }
+    // placement: column pointers in node-id order, the copy and the vectors, one pass
     if (N > 0) {
-        const int64_t warps = std::min<int64_t>(((int64_t)N + 31) / 32, (int64_t)ctx->sm_count * 64);
-        k4_place<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(p, wtc, labp, ffscan);
+        const int64_t ptiles = ((int64_t)N + kPlaceThreads - 1) / kPlaceThreads;
+        FL_TRY(res->v4[2].ensure(sizeof(uint64_t) * (size_t)(ptiles + 2)));
+        uint64_t* status = res->v4[2].as<uint64_t>();
+        FL_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)(ptiles + 2), s));
+        unsigned int* ticket = reinterpret_cast<unsigned int*>(status + ptiles + 1);
+        k4_place<<<(int)ptiles, kPlaceThreads, 0, s>>>(p, wtc, lp.lab.as<int32_t>(), status, ticket);
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());

@@ -312,7 +312,7 @@ __global__ void k_validate(int32_t n_elems, int32_t n_nodes, const double* __res
 // (mesh.hpp:222-246).  is_dir[v] = 1 for every vertex of a flag-1 face.
 // ===========================================================================
 template <int D>
-__global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ elems,
+__global__ void k_mark_boundary(int32_t n_elems, int32_t n_nodes, const int32_t* __restrict__ elems,
                                 const int8_t* __restrict__ flags, int8_t* __restrict__ is_dir,
                                 int8_t* __restrict__ is_neu, uint32_t* __restrict__ counters) {
     constexpr int NV = D + 1;
@@ -328,8 +328,13 @@ __global__ void k_mark_boundary(int32_t n_elems, const int32_t* __restrict__ ele
         if (f == 1) ++dir_faces;
         else ++neu_faces;
 #pragma unroll
-        for (int k = 0; k < NV; ++k)
-            if (k != lf) mark[elems[(size_t)t * NV + k]] = 1;
+        for (int k = 0; k < NV; ++k) {
+            if (k == lf) continue;
+            // a vertex id outside [0, N) is reported (index_out_of_range), never written
+            const int32_t v = elems[(size_t)t * NV + k];
+            if ((uint32_t)v < (uint32_t)n_nodes) mark[v] = 1;
+            else err |= DERR_INDEX;
+        }
     };
     // 16 flags per load: nearly all are 0 (interior faces)
     const int64_t n_vec = n_entries >> 4;
@@ -1522,10 +1527,10 @@ int launch_partition(fl_ctx* ctx, fl_mesh* mesh, fl_result* res) {
     if (mesh->has_flags && n_entries > 0) {
         const int grid = (int)std::min<int64_t>(div_up(n_entries, 256), (int64_t)ctx->sm_count * 16);
         if (mesh->dim == 2)
-            k_mark_boundary<2><<<grid, 256, 0, s>>>(mesh->n_elems, mesh->elems.as<int32_t>(),
+            k_mark_boundary<2><<<grid, 256, 0, s>>>(mesh->n_elems, N, mesh->elems.as<int32_t>(),
                                                    mesh->flags.as<int8_t>(), is_dir, is_neu, counters);
         else
-            k_mark_boundary<3><<<grid, 256, 0, s>>>(mesh->n_elems, mesh->elems.as<int32_t>(),
+            k_mark_boundary<3><<<grid, 256, 0, s>>>(mesh->n_elems, N, mesh->elems.as<int32_t>(),
                                                    mesh->flags.as<int8_t>(), is_dir, is_neu, counters);
         count_launch(ctx);
     }

@@ -106,6 +106,55 @@ def stitch_csc(m: int, parts: Sequence[tuple[np.ndarray, np.ndarray, np.ndarray]
     return CscMatrix(m, col_ptr.size - 1, col_ptr, row_idx, values)
 
 
+def gather_csc_to_root(info: "ShardInfo", col_ptr, row_idx, values, root: int = 0, group=None):
+    """The verification gather to `root` (SURVEY.md §8(e) collective 2): grouped
+    point-to-point sends of every rank's column shard -- col_ptr[1:], row_idx,
+    values -- received straight into their slices of the global arrays (NCCL
+    send/recv between GPU tensors; gloo moves CPU tensors).  Root then shifts
+    each shard's pointers by the nnz of the ranks before it.  Returns the global
+    (col_ptr, row_idx, values) tensors on root, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    off = info.offsets
+    cp_l, ri_l, va_l = col_ptr, row_idx, values
+    if rank != root:
+        ops = []
+        if int(info.counts[rank, 0]) > 0:
+            ops.append(dist.P2POp(dist.isend, cp_l[1:].contiguous(), root, group))
+        if int(info.counts[rank, 2]) > 0:
+            ops.append(dist.P2POp(dist.isend, ri_l.contiguous(), root, group))
+            ops.append(dist.P2POp(dist.isend, va_l.contiguous(), root, group))
+        for req in (dist.batch_isend_irecv(ops) if ops else []):
+            req.wait()
+        return None
+    n, nnz = int(off[-1, 0]), int(off[-1, 2])
+    dev = ri_l.device
+    cp = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+    ri = torch.empty(nnz, dtype=torch.int32, device=dev)
+    va = torch.empty(nnz, dtype=torch.float64, device=dev)
+    ops = []
+    for r in range(world):
+        c0, c1, z0, z1 = int(off[r, 0]), int(off[r + 1, 0]), int(off[r, 2]), int(off[r + 1, 2])
+        if r == root:
+            cp[c0 + 1:c1 + 1] = cp_l[1:]
+            ri[z0:z1] = ri_l
+            va[z0:z1] = va_l
+            continue
+        if c1 > c0:
+            ops.append(dist.P2POp(dist.irecv, cp[c0 + 1:c1 + 1], r, group))
+        if z1 > z0:
+            ops.append(dist.P2POp(dist.irecv, ri[z0:z1], r, group))
+            ops.append(dist.P2POp(dist.irecv, va[z0:z1], r, group))
+    for req in (dist.batch_isend_irecv(ops) if ops else []):
+        req.wait()
+    for r in range(world):
+        c0, c1, z0 = int(off[r, 0]), int(off[r + 1, 0]), int(off[r, 2])
+        if z0:
+            cp[c0 + 1:c1 + 1] += z0
+    return cp, ri, va
+
+
 def gather_to_root(obj, root: int = 0, group=None):
     """Host objects of all ranks on `root` (list in rank order), None elsewhere."""
     import torch.distributed as dist

@@ -18,6 +18,7 @@ import paper_1804_05156_b200 as fl
 from paper_1804_05156_b200 import _lib
 from paper_1804_05156_b200.mesh import Mesh
 from paper_1804_05156_b200.shard import ShardedAssembler, column_ranges, exclusive_offsets, stitch_csc
+from oracle import pyoracle as po
 
 pytestmark = pytest.mark.gpu
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
@@ -198,3 +199,34 @@ def test_result_counts_async_matches_sizes(world, ctx):
         _lib.check(_lib.lib().fl_result_counts_async(res.handle, C.c_void_p(out.data_ptr())))
         ctx.synchronize()
         assert out.cpu().tolist() == [s.n, s.n_free_cols, s.nnz, s.nnz_ff]
+
+
+def test_bench_two_ranks_gather_gloo(tmp_path, ref_which):
+    """bench.py --gpus 2 under torchrun on ONE GPU with FL_BENCH_BACKEND=gloo (a
+    functional check of the sharded path: both ranks share cuda:0, so the numbers
+    mean nothing): the grouped send/recv verification gather to rank 0
+    (shard.gather_csc_to_root, NCCL on a real multi-GPU run) reassembles the
+    reference's A bit for bit."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    from paper_1804_05156_b200 import configs
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "gathered.npz"
+    env = dict(os.environ, FL_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+           "--config", "C2", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
+           "--no-cached", "--dump-gather", str(out)]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    g = np.load(out)
+    m = configs.build("C2").mesh
+    a = po.assemble_blockwise(m.dim, m.nodes, m.elems, which=ref_which)
+    np.testing.assert_array_equal(g["col_ptr"], a.col_ptr)
+    np.testing.assert_array_equal(g["row_idx"], a.row_idx)
+    assert g["values"].tobytes() == a.values.tobytes()

@@ -2,7 +2,8 @@
 
 Two processes over gloo (127.0.0.1) run exactly the host logic the GPU ranks
 run in bench.py / ShardedAssembler.finish: column ranges, the all_gather of the
-per-shard counts, offsets, and the gather + stitch on rank 0.  The per-rank
+per-shard counts, offsets, and the point-to-point gather to rank 0 (the
+same grouped send/recv the GPU ranks run over NCCL).  The per-rank
 column assembly is the oracle's column-subset restatement (the GPU path is
 covered by tests/test_gpu_shard.py); rank 0 checks the stitched matrix, the
 offsets and the free-column split against the reference's golden fixture.
@@ -43,7 +44,10 @@ def _worker(rank, world, port, tag, q):
         counts = shard.exchange_counts([c1 - c0, free_cols.size, sub.nnz, 0])
         off = shard.exclusive_offsets(counts)
         info = shard.ShardInfo(rank, world, c0, c1, counts, off)
-        parts = shard.gather_to_root((sub.col_ptr, sub.row_idx, sub.values))
+        import torch
+        gathered = shard.gather_csc_to_root(info, torch.from_numpy(np.ascontiguousarray(sub.col_ptr, np.int32)),
+                                            torch.from_numpy(np.ascontiguousarray(sub.row_idx, np.int32)),
+                                            torch.from_numpy(np.ascontiguousarray(sub.values, np.float64)))
         ok = True
         msg = ""
         # every rank agrees on its global offsets
@@ -51,10 +55,10 @@ def _worker(rank, world, port, tag, q):
         ok &= info.free_before == int(np.searchsorted(free, c0))
         ok &= info.nnz_total == int(g["a_col_ptr"][-1])
         if rank == 0:
-            full = shard.stitch_csc(n, parts)
-            ok &= np.array_equal(full.col_ptr, g["a_col_ptr"])
-            ok &= np.array_equal(full.row_idx, g["a_row_idx"])
-            ok &= full.values.tobytes() == g["a_values"].tobytes()
+            cp, ri, va = (t.numpy() for t in gathered)
+            ok &= np.array_equal(cp, g["a_col_ptr"])
+            ok &= np.array_equal(ri, g["a_row_idx"])
+            ok &= va.tobytes() == g["a_values"].tobytes()
             ok &= int(off[-1, 1]) == free.size
             if not ok:
                 msg = "stitched matrix differs"

@@ -4,7 +4,8 @@
 reads gpurun_out/ll_<cfg>.csv (launch lists: gpu__time_duration.sum +
 dram bytes per kernel, one assemble_system step, ncu --clock-control none)
 and writes profiles/<tag>_launches_<cfg>.txt plus profiles/traffic.json
-(numeric-phase dram bytes per step, read by bench.py as roofline.traffic).
+(dram bytes of the whole step and of the column kernel k_columns4, read by
+bench.py as roofline.traffic / roofline.dominant_kernel.traffic).
 """
 import collections
 import csv
@@ -13,7 +14,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NUMERIC = ("k_elem_records", "k_columns", "k_stage_copy", "finish_staging")
+DOMINANT = "k_columns4"
 tag = sys.argv[1]
 traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
 traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
@@ -28,16 +29,19 @@ for c in sys.argv[2:]:
     lines = [f"# {c}: one assemble_system step (FL_OUT_SYSTEM|plan), ncu --clock-control none,",
              "# serialized cold-cache launches; time share is what matters, not the absolute",
              f"{'id':>3} {'kernel':60s} {'time_us':>10} {'share':>6} {'dram_rd_MB':>11} {'dram_wr_MB':>11}"]
-    num_bytes, num_t = 0.0, 0.0
+    step_bytes, kern_bytes, kern_t = 0.0, 0.0, 0.0
     for (i, k), m in sorted(d.items()):
         t = m.get("gpu__time_duration.sum", 0)
         rd, wr = m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
         lines.append(f"{i:3d} {k[:60]:60s} {t/1e3:10.1f} {100*t/tot:5.1f}% {rd/1e6:11.1f} {wr/1e6:11.1f}")
-        if any(s in k for s in NUMERIC):
-            num_bytes += rd + wr
-            num_t += t
-    lines.append(f"# total {tot/1e6:.3f} ms; numeric phase {num_t/1e6:.3f} ms, dram {num_bytes/1e9:.3f} GB")
+        step_bytes += rd + wr
+        if DOMINANT in k:
+            kern_bytes += rd + wr
+            kern_t += t
+    lines.append(f"# total {tot/1e6:.3f} ms, dram {step_bytes/1e9:.3f} GB; {DOMINANT} {kern_t/1e6:.3f} ms "
+                 f"({100*kern_t/max(tot,1):.1f}%), dram {kern_bytes/1e9:.3f} GB")
     open(os.path.join(ROOT, "profiles", f"{tag}_launches_{c}.txt"), "w").write("\n".join(lines) + "\n")
-    traffic[c] = {"dram_bytes": num_bytes, "source": f"profiles/{tag}_launches_{c}.txt (ncu dram__bytes_read.sum+write.sum, numeric-phase kernels)"}
+    traffic[c] = {"step_dram_bytes": step_bytes, "kernel_dram_bytes": kern_bytes,
+                  "source": f"profiles/{tag}_launches_{c}.txt (ncu dram__bytes_read.sum+write.sum per step)"}
     print("\n".join(lines[-3:]))
 json.dump(traffic, open(traffic_path, "w"), indent=1)

@@ -13,10 +13,12 @@ python bench.py --impl reference > gpurun_out/f_ref.json 2> gpurun_out/f_ref.err
 for c in C1 C2 C3 C4 C5; do python tools/one_step.py $c 1 > /dev/null 2>&1; done
 bash tools/launch_list.sh C1 C2 C3 C4 C5
 python tools/one_step.py C5 1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_columns3 -c 1 \
-      -o gpurun_out/full_k_columns3_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_elem_records -c 1 \
-      -o gpurun_out/full_k_elem_records_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_inc_fill -c 1 \
-      -o gpurun_out/full_k_inc_fill_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full3.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_columns4 -c 1 \
+      -o gpurun_out/full_k_columns4_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_columns4 -c 1 \
+      -o gpurun_out/full_k_columns4_C4 python tools/one_step.py C4 1 > gpurun_out/ncu_full2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k4_fill -c 1 \
+      -o gpurun_out/full_k4_fill_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k4_place -c 1 \
+      -o gpurun_out/full_k4_place_C5 python tools/one_step.py C5 1 > gpurun_out/ncu_full4.log 2>&1
 ls -la gpurun_out
