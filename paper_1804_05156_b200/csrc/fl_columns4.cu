@@ -42,6 +42,7 @@
 namespace fl {
 
 constexpr unsigned kFull = 0xffffffffu;
+__host__ __device__ constexpr int lg2c(int x) { return x <= 1 ? 0 : 1 + lg2c(x >> 1); }
 
 // ===========================================================================
 // plan
@@ -302,6 +303,104 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, const int32_
     }
 }
 
+// ---- block-sorted fill (FL_PLAN=s; measured SLOWER than the direct fill on C5,
+// 5.58 vs 3.64 ms: the shared-memory hash, its scan and 40 KB of shared memory
+// per block cost more than the scattered stores it saves).  A block takes
+// 2048 consecutive entries; their labels repeat ~6 times (a node's incident
+// elements are neighbours in the element stream), so the block groups its
+// entries by label in shared memory (hash of labels), reserves each label's run
+// with ONE global atomic, and writes the keys out in label order: consecutive
+// threads store consecutive slots of a run instead of 32 scattered keys per
+// store instruction.  Slot order inside a run is arbitrary either way (the
+// column kernel sorts its keys).
+constexpr int kSF = 8;                       // entries per thread
+constexpr int kSFChunk = kP4Block * kSF;     // 2048 entries per block
+constexpr int kSFHash = 2048;                // label hash slots (power of 2, >= entries per block)
+
+__global__ void __launch_bounds__(kP4Block)
+k4_fill_sorted(int64_t n_entries, int nv, int32_t n_nodes, const int32_t* __restrict__ elems,
+               const int32_t* __restrict__ lab, int32_t* __restrict__ cursor, uint32_t* __restrict__ linc,
+               int32_t* __restrict__ lel) {
+    __shared__ int32_t hkey[kSFHash];
+    __shared__ int32_t hcnt[kSFHash];  // count, then the run's first sorted position
+    __shared__ int32_t hbase[kSFHash]; // the run's first global slot
+    __shared__ int2 sorted[kSFChunk];  // (global slot, key) in label order
+    __shared__ int32_t wsum[kP4Block / 32];
+    const int tid = threadIdx.x;
+    const int64_t e0 = (int64_t)blockIdx.x * kSFChunk;
+    for (int h = tid; h < kSFHash; h += kP4Block) {
+        hkey[h] = -1;
+        hcnt[h] = 0;
+    }
+    __syncthreads();
+    int32_t slot[kSF], rank[kSF];
+    uint32_t key[kSF];
+#pragma unroll
+    for (int k = 0; k < kSF; ++k) {
+        const int64_t e = e0 + (int64_t)k * kP4Block + tid;
+        slot[k] = -1;
+        if (e < n_entries) {
+            const int32_t v = __ldg(elems + e);
+            const int32_t lb = (uint32_t)v < (uint32_t)n_nodes ? __ldg(lab + v) : -1;
+            lel[e] = lb;
+            if (lb >= 0) {
+                const int32_t t = (int32_t)(e / nv);
+                key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
+                uint32_t h = ((uint32_t)lb * 2654435761u) >> (32 - lg2c(kSFHash));
+                while (true) {  // the table holds <= 2048 labels: always finds a slot
+                    const int32_t old = atomicCAS(&hkey[h], -1, lb);
+                    if (old == -1 || old == lb) break;
+                    h = (h + 1) & (kSFHash - 1);
+                }
+                slot[k] = (int32_t)h;
+                rank[k] = atomicAdd(&hcnt[h], 1);
+            }
+        }
+    }
+    __syncthreads();
+    // runs in slot order: exclusive scan of the counts over the table
+    constexpr int PER = kSFHash / kP4Block;  // slots per thread (contiguous)
+    int32_t c[PER], tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        c[q] = hcnt[tid * PER + q];
+        tot += c[q];
+    }
+    const int lane = tid & 31, w = tid >> 5;
+    int32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int32_t before = 0, nsorted = 0;
+    for (int i = 0; i < kP4Block / 32; ++i) {
+        if (i < w) before += wsum[i];
+        nsorted += wsum[i];
+    }
+    int32_t run = before + incl - tot;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int h = tid * PER + q;
+        if (c[q]) {
+            hbase[h] = atomicAdd(cursor + hkey[h], c[q]);  // one reservation per label
+            hcnt[h] = run;
+        }
+        run += c[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSF; ++k)
+        if (slot[k] >= 0) sorted[hcnt[slot[k]] + rank[k]] = make_int2(hbase[slot[k]] + rank[k], (int32_t)key[k]);
+    __syncthreads();
+    for (int q = tid; q < nsorted; q += kP4Block) {
+        const int2 x = sorted[q];
+        linc[x.x] = (uint32_t)x.y;
+    }
+}
+
 // ---- bucketed fill (large 2-D meshes, element order not spatial: C3).  The
 // direct fill scatters 4-byte keys over the whole incidence array there, each a
 // sector read-modify-write.  Instead: (1) partition (label, key) pairs into
@@ -406,7 +505,6 @@ __global__ void k4_xl(int32_t n, int dim, const int32_t* __restrict__ ilab, cons
 // ===========================================================================
 // column kernel
 // ===========================================================================
-__host__ __device__ constexpr int lg2c(int x) { return x <= 1 ? 0 : 1 + lg2c(x >> 1); }
 
 template <int D, int L, int K>
 struct V4 {
@@ -790,7 +888,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
             const double b = __shfl_sync(kFull, fold, 0, L);
             const double dg = __shfl_sync(kFull, fold, 1, L);
             double ylift = 0.0;
-            uint64_t meta = 0;  // staging: in-tile offset | count of A, then of A(free, free)
+            uint64_t meta = 0;  // staging: first entry (40 bits) | count of A | count of A(free, free)
             if (p.want_a) {
                 // ---- 4. the diagonal slot, the folds, rows ranked, zero drop
                 if (g == 0 && act && m > 0) {
@@ -915,7 +1013,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                     }
                     const int tot_a = __shfl_sync(kFull, pa, 31);
                     const int wa = run_a + pa - na;  // this column's first slot
-                    meta = (uint64_t)wa | ((uint64_t)na << 16) | ((uint64_t)nf << 24);
+                    meta = (uint64_t)(sbase + wa) | ((uint64_t)na << 40) | ((uint64_t)nf << 48);
 #pragma unroll
                     for (int ii = 0; ii < NI; ++ii) {
                         const int rk = rkv[ii];
@@ -1001,7 +1099,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 }
                 const int tot_a = __shfl_sync(kFull, pa, 31);
                 int wa = run_a + pa - na;  // this column's first slot
-                meta = (uint64_t)wa | ((uint64_t)na << 16) | ((uint64_t)nf << 24);
+                meta = (uint64_t)(sbase + wa) | ((uint64_t)na << 40) | ((uint64_t)nf << 48);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     const int qq = ch * L + g;
@@ -1021,14 +1119,15 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 run_a += tot_a;
                 }  // LIFT
             }
-            // ---- per-column vectors, by label: {b, u0, b - A u0}
+            // ---- per-column record, by NODE ID (the placement then streams it):
+            //      {b, u0, b - A u0, staging meta}
             if (act && g == 0) {
                 double u0 = 0.0, bmod = b;
                 if (p.want_sys) {
                     u0 = fc_c < 0 ? node_field4(p.g_dir, p.nodes, D, c) : 0.0;
                     bmod = LIFT ? b - ylift : b - 0.0;  // system.hpp:197-198
                 }
-                p.vst[l] = make_double4(b, u0, bmod, __longlong_as_double((long long)meta));
+                p.vst[c] = make_double4(b, u0, bmod, __longlong_as_double((long long)meta));
             }
             __syncwarp();
         }
@@ -1040,16 +1139,15 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
 // placement: label-ordered staging -> node-id-ordered CSC and vectors, one pass
 // ===========================================================================
 // Tile = 256 consecutive node ids (one per thread), tiles taken in order from a
-// ticket.  Each node's label record vst[lab[v]] holds its vectors and, packed in
-// .w, the in-tile staging offset and count of its A and A(free, free) entries
-// (meta of k_columns4).  The column pointers are an exclusive scan over node ids
+// ticket.  Each node's record vst[v] (written by k_columns4 at the node id) holds
+// its vectors and, packed in .w, the staging index and count of its A and
+// A(free, free) entries.  The column pointers are an exclusive scan over node ids
 // (block scan + decoupled look-back on (nnz_A, nnz_Aff) packed in 64 bits); a
 // warp's 32 consecutive columns are one contiguous destination run, copied with
 // every store instruction writing 32 consecutive entries.
 constexpr int kPlaceThreads = 256;
 
-__global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, int wtc, const int32_t* __restrict__ lab,
-                                                          uint64_t* __restrict__ status,
+__global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t* __restrict__ status,
                                                           unsigned int* __restrict__ ticket) {
     __shared__ int64_t warp_sums[kPlaceThreads / 32];
     __shared__ int64_t s_tile, s_excl;
@@ -1060,14 +1158,13 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, int wtc, 
     const int64_t tile = s_tile;
     const int32_t v = (int32_t)(tile * kPlaceThreads) + threadIdx.x;
     const bool in = v < N;
-    const int32_t l = in ? __ldg(lab + v) : 0;
     const int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + v) : -1;
     double4 vs = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (in) vs = ld_xl(p.vst + l);
+    if (in) vs = ld_xl(p.vst + v);  // the record of node v, in node order
     const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
-    const int32_t ca = in ? (int32_t)((meta >> 16) & 0xFF) : 0;
-    const int32_t cf = fr >= 0 ? (int32_t)((meta >> 24) & 0xFF) : 0;
-    const int64_t src = (int64_t)(l / wtc) * p.tile_cap + (int64_t)(meta & 0xFFFF);
+    const int32_t ca = in ? (int32_t)((meta >> 40) & 0xFF) : 0;
+    const int32_t cf = fr >= 0 ? (int32_t)((meta >> 48) & 0xFF) : 0;
+    const int64_t src = (int64_t)(meta & 0xFFFFFFFFFFull);
     if (in) {
         if (p.want_b) p.b[v] = vs.x;
         if (p.want_sys) {
@@ -1247,7 +1344,13 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         const int bgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, kP4Block * 4), 1), INT_MAX);
         k4_fill_b<<<bgrid, kP4Block, 0, s>>>(lp.lptr.as<int32_t>() + N, stg, cnt, lp.linc.as<uint32_t>());
         count_launch(ctx);
-    } else if (n_entries > 0) {
+    } else if (n_entries > 0 && penv && penv[0] == 's') {
+        // FL_PLAN=s: block-sorted fill (measured slower on C5: 5.58 vs 3.64 ms)
+        const int64_t chunks = (n_entries + kSFChunk - 1) / kSFChunk;
+        k4_fill_sorted<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, mesh->elems.as<int32_t>(), lab, cnt,
+                                                        lp.linc.as<uint32_t>(), lp.lel.as<int32_t>());
+        count_launch(ctx);
+    } else if (n_entries > 0) {  // the direct fill (one key per store)
         constexpr int U = 4;
         const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
         k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, mesh->elems.as<int32_t>(), lab, cnt,
@@ -1362,7 +1465,7 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
         uint64_t* status = res->v4[2].as<uint64_t>();
         FL_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)(ptiles + 2), s));
         unsigned int* ticket = reinterpret_cast<unsigned int*>(status + ptiles + 1);
-        k4_place<<<(int)ptiles, kPlaceThreads, 0, s>>>(p, wtc, lp.lab.as<int32_t>(), status, ticket);
+        k4_place<<<(int)ptiles, kPlaceThreads, 0, s>>>(p, status, ticket);
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
