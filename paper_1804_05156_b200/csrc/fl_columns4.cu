@@ -1287,10 +1287,13 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
             count_launch(ctx);
         }
     } else if (N > 0) {
-        // Morton cells of ~64 nodes: 2^(dim*bits) cells
+        // Morton cells of ~cn nodes (FL_CELL_NODES, default 8: C5 column pass 18.2 / 17.8
+        // / 17.7 ms at 64 / 8 / 1, plan +0.6 ms at 1): 2^(dim*bits) cells
         const int dim = mesh->dim;
+        const char* cenv = std::getenv("FL_CELL_NODES");
+        const int64_t cn = cenv ? std::max(1, std::atoi(cenv)) : 8;
         int bits = 1;
-        while (bits < (dim == 3 ? 10 : 15) && ((int64_t)1 << (dim * (bits + 1))) * 64 <= (int64_t)N) ++bits;
+        while (bits < (dim == 3 ? 10 : 15) && ((int64_t)1 << (dim * (bits + 1))) * cn <= (int64_t)N) ++bits;
         const int64_t ncell = (int64_t)1 << (dim * bits);
         const int nparts = std::min(div_up(N, 256), ctx->sm_count * 4);
         FL_TRY(lp.cells.ensure(sizeof(int32_t) * ((size_t)N + 2 * (size_t)ncell + 2) + sizeof(double) * (6 * (size_t)nparts + 1)));

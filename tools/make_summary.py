@@ -1,47 +1,65 @@
-"""profiles/<tag>_summary.md from gpurun_out/f_<cfg>.json bench lines (+ f_ref.json)."""
+"""profiles/<tag>_summary.md from bench lines.
+
+  python tools/make_summary.py <tag> [prefix]     (default prefix: ev_)
+reads gpurun_out/<prefix>bench_<cfg>.json, <prefix>ref.json and
+<prefix>ref_full_c5.json (tools/runs/evidence.sh)."""
 import json
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
-rows = []
-for c in ["C1", "C2", "C3", "C4", "C5"]:
-    p = os.path.join(ROOT, "gpurun_out", f"f_{c}.json")
+pre = sys.argv[2] if len(sys.argv) > 2 else "ev_"
+
+
+def load(name):
+    p = os.path.join(ROOT, "gpurun_out", name)
     if not os.path.exists(p):
-        continue
-    d = json.loads(open(p).read().strip().splitlines()[-1])
-    rows.append((c, d))
-out = [f"# {tag}: bench.py results on one B200 (N=1)", "",
-       "Each line: `python bench.py --config Cx` (defaults: 10 timed steps after 3 warm-up;"
-       " step = plan + partition + stiffness + load + Dirichlet lift + A(free,free) + b_f)."
-       " Device numbers are CUDA-event times with inputs resident in HBM; e2e is wall clock"
-       " through the C-ABI from pinned host memory (3-deep pipeline of contexts); cpu = the"
-       " reference's own CPU path (oracle/_ref, 1 thread) on the config's bounded sample.", "",
-       "| cfg | workload | NT | ms/step | Gelem/s | e2e Gelem/s | cpu Melem/s | e2e / cpu | numeric-phase GB/s (frac of 6547.8) | plan / partition / records / column kernel / placement ms | clocks |",
+        return None
+    lines = [l for l in open(p).read().strip().splitlines() if l.startswith("{")]
+    return json.loads(lines[-1]) if lines else None
+
+
+out = [f"# {tag}: bench.py on one B200 (N=1)", "",
+       "`python bench.py --config Cx` (10 timed steps after 3 warm-up). Step = Morton labels + label "
+       "plan rebuilt from the raw arrays + partition + FaceLists + stiffness + load + Dirichlet lift + "
+       "A(free,free) + b_f (`fl_assemble(FL_OUT_SYSTEM|FL_REPLAN)`). Device numbers: CUDA events, inputs "
+       "resident in HBM. `frac` = B_SL / step / measured HBM peak (SURVEY §8(d)). e2e: C-ABI from pinned "
+       "host memory, 3-deep pipeline; e2e 1-call: one un-pipelined call. cpu: the reference's own path "
+       "(oracle/_ref) on all host threads, bounded sample of the config family.", "",
+       "| cfg | NT | ms/step | Gelem/s | frac (B_SL) | e2e Gelem/s | e2e 1-call ms | cpu Melem/s (threads) | "
+       "labels+plan / partition+faces / xl+column / placement ms | column kernel ms (share) | clocks |",
        "|---|---|---|---|---|---|---|---|---|---|---|"]
-for c, d in rows:
+for c in ["C1", "C2", "C3", "C4", "C5"]:
+    d = load(f"{pre}bench_{c}.json")
+    if not d:
+        continue
     ph = d["phases_ms"]
-    cpu = d.get("cpu_baseline")
-    cpu_v = cpu["value"] / 1e6 if cpu else None
-    e2e = d["e2e"]["value"] / 1e9 if d.get("e2e") else None
-    ratio = f"{d['e2e']['value'] / cpu['value']:.0f}x" if cpu and d.get("e2e") else "-"
-    out.append(f"| {c} | {d['config']['workload']} | {d['config']['n_elems']:,} | {d['ms_per_step']:.3f} | "
-               f"{d['value'] / 1e9:.3f} | {e2e:.3f} | {cpu_v:.3f} | {ratio} | "
-               f"{d['roofline']['achieved']:.0f} ({d['roofline']['frac']:.3f}) | "
-               f"{ph['plan']:.3f} / {ph['partition']:.3f} / {ph['element_records']:.3f} / "
-               f"{ph['column_kernel']:.3f} / {ph['placement']:.3f} | "
-               f"{d['clocks']['sm_mhz']} MHz {d['clocks']['reasons']} |"
-               if cpu_v is not None and e2e is not None else
-               f"| {c} | {d['config']['workload']} | {d['config']['n_elems']:,} | {d['ms_per_step']:.3f} | "
-               f"{d['value'] / 1e9:.3f} | {e2e} | - | - | {d['roofline']['achieved']:.0f} "
-               f"({d['roofline']['frac']:.3f}) | {ph['plan']:.3f} / {ph['partition']:.3f} / "
-               f"{ph['element_records']:.3f} / {ph['column_kernel']:.3f} / {ph['placement']:.3f} | "
-               f"{d['clocks']['sm_mhz']} MHz {d['clocks']['reasons']} |")
-p = os.path.join(ROOT, "gpurun_out", "f_ref.json")
-if os.path.exists(p):
-    d = json.loads(open(p).read().strip().splitlines()[-1])
-    out += ["", f"`bench.py --impl reference`: {d['value'] / 1e6:.3f} Melem/s, {d['ms_per_step']:.1f} ms per "
-            f"sample step ({d['cpu_baseline']['sample']})."]
+    cpu = d.get("cpu_baseline") or {}
+    e2e = d.get("e2e") or {}
+    single = d.get("e2e_single") or {}
+    dk = d["roofline"].get("dominant_kernel", {})
+    out.append(
+        f"| {c} | {d['config']['n_elems']:,} | {d['ms_per_step']:.3f} | {d['value'] / 1e9:.3f} | "
+        f"{d['roofline']['frac']:.4f} | {e2e.get('value', 0) / 1e9:.3f} | {single.get('ms', 0):.1f} | "
+        f"{cpu.get('value', 0) / 1e6:.2f} ({cpu.get('cores', '-')}) | "
+        f"{ph['plan']:.3f} / {ph['partition']:.3f} / {ph['numeric'] - ph['placement']:.3f} / {ph['placement']:.3f} | "
+        f"{ph['column_kernel']:.3f} ({dk.get('share_of_step') or 0:.0%}) | "
+        f"{d['clocks']['sm_mhz']} MHz {d['clocks']['reasons']} |")
+r = load(f"{pre}ref.json")
+if r:
+    out += ["", f"`bench.py --impl reference`: {r['value'] / 1e6:.3f} Melem/s, {r['ms_per_step']:.1f} ms per "
+            f"sample round on {r['cpu_baseline']['cores']} threads ({r['cpu_baseline']['sample']})."]
+f = load(f"{pre}ref_full_c5.json")
+if f:
+    s = f["sample"]
+    line = (f"\nThe reference on one thread (`tools/ref_full_c5.py`, {f.get('cpu_model', '')}): sample "
+            f"unit_cube:64 {s['elements_per_s'] / 1e6:.3f} Melem/s ({s['seconds']:.1f} s)")
+    if "full" in f:
+        g = f["full"]
+        line += (f"; FULL C5 unit_cube:256 {g['elements_per_s'] / 1e6:.3f} Melem/s ({g['seconds']:.1f} s, "
+                 f"peak RSS {f.get('peak_rss_gb') or 0:.1f} GB): full/sample per-element rate "
+                 f"{f['full_over_sample_rate']:.2f}.")
+    out.append(line)
 open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
