@@ -303,7 +303,11 @@ FL_API int fl_mesh_set_columns(fl_ctx* ctx, fl_mesh* mesh, int32_t col_begin, in
     if (!ctx || !mesh) return set_error(FL_ERR_ARGUMENT, "null argument");
     if (col_begin < 0 || col_end < col_begin || col_end > mesh->n_nodes)
         return set_error(FL_E_INDEX_OUT_OF_RANGE, "column range outside [0, n_nodes]");
-    if (col_begin != mesh->col_begin || col_end != mesh->col_end) mesh->planned = false;
+    if (col_begin != mesh->col_begin || col_end != mesh->col_end) {
+        mesh->planned = false;
+        mesh->lp.planned = false;  // the label plan orders the owned columns first
+        mesh->lp.ever = false;     // and its bounds are the old range's: plan synchronously
+    }
     mesh->col_begin = col_begin;
     mesh->col_end = col_end;
     return FL_OK;
@@ -473,14 +477,14 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     const bool need_plan = what & (FL_OUT_STIFFNESS | FL_OUT_LOAD);
     const char* kern = std::getenv("FL_KERNEL");
     const char kk = kern ? kern[0] : '0';
-    // the label-space pipeline (fl_columns4.cu) takes whole meshes without
-    // Neumann data whose valence fits its kernel; FL_V4=0 forces the id-space one
+    // the label-space pipeline (fl_columns4.cu) takes meshes (whole or a column
+    // range) without Neumann data whose valence fits its kernel; FL_V4=0 forces
+    // the id-space one
     const char* v4env = std::getenv("FL_V4");
     const bool neu_data = (what & FL_OUT_LOAD) && mesh->has_flags && g_neumann &&
                           g_neumann->kind != FL_FIELD_NONE;
-    bool use_v4 = need_plan && kk == '0' && !(v4env && v4env[0] == '0') && mesh->col_begin == 0 &&
-                  mesh->col_end == mesh->n_nodes && mesh->n_nodes > 0 && mesh->n_elems > 0 &&
-                  mesh->lp.ok && !neu_data;
+    bool use_v4 = need_plan && kk == '0' && !(v4env && v4env[0] == '0') && mesh->n_nodes > 0 &&
+                  mesh->n_elems > 0 && mesh->lp.ok && !neu_data;
     if (use_v4 && (replan || !mesh->lp.planned)) {
         // a re-plan runs asynchronously with the previous bounds (fl_result_sizes
         // refreshes them and reruns on the general kernel if they were exceeded)

@@ -198,8 +198,12 @@ __device__ __forceinline__ uint32_t spread2(uint32_t x) {  // 15 bits -> every s
 }
 
 // cell of every node (Morton code of its quantised coordinates) and per-cell counts
+// A column range [c0, c1) (multi-GPU shard) puts the nodes outside it into a
+// second run of cells: the owned nodes take labels [0, c1 - c0), still in Morton
+// order, and every other node keeps a label for its xl record.
 __global__ void k4_cell(int32_t n, int dim, int bits, int nparts, const double* __restrict__ nodes,
-                        const double* __restrict__ part, int32_t* __restrict__ cell, int32_t* __restrict__ ccnt) {
+                        const double* __restrict__ part, int32_t c0, int32_t c1, int32_t* __restrict__ cell,
+                        int32_t* __restrict__ ccnt) {
     __shared__ double box[6];
     if (threadIdx.x < 6) {
         double r = part[threadIdx.x];
@@ -218,8 +222,9 @@ __global__ void k4_cell(int32_t n, int dim, int bits, int nparts, const double* 
             const double f = (x - box[d]) * sc[d];
             q[d] = f > 0.0 ? min((uint32_t)f, qmax) : 0u;  // NaN coordinates land in cell 0
         }
-        const uint32_t code = dim == 3 ? (spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2))
-                                       : (spread2(q[0]) | (spread2(q[1]) << 1));
+        uint32_t code = dim == 3 ? (spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2))
+                                 : (spread2(q[0]) | (spread2(q[1]) << 1));
+        if (v < c0 || v >= c1) code += 1u << (dim * bits);
         cell[v] = (int32_t)code;
         atomicAdd(ccnt + code, 1);
     }
@@ -237,8 +242,8 @@ __global__ void k4_cell_scatter(int32_t n, const int32_t* __restrict__ cell, int
 
 // incidence counts per node (label-free count pass of the spatial labelling)
 __global__ void __launch_bounds__(kP4Block)
-k4_count_plain(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ elems, int32_t* __restrict__ cnt,
-               P4Misc* __restrict__ misc) {
+k4_count_plain(int64_t n_entries, int32_t n_nodes, int32_t c0, int32_t c1, const int32_t* __restrict__ elems,
+               int32_t* __restrict__ cnt, P4Misc* __restrict__ misc) {
     const unsigned lower = (1u << (threadIdx.x & 31)) - 1;
     const int64_t b0 = (int64_t)blockIdx.x * kP4Block * kP4Iters;
     uint32_t err = 0;
@@ -249,7 +254,7 @@ k4_count_plain(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ e
         if (e < n_entries) {
             const int32_t v = __ldg(elems + e);
             if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
-            else key = v;
+            else if (v >= c0 && v < c1) key = v;  // columns of this shard
         }
         const unsigned g = __match_any_sync(kFull, key);
         if (key >= 0 && (g & lower) == 0) atomicAdd(cnt + key, __popc(g));
@@ -262,11 +267,12 @@ k4_count_plain(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ e
 // one warp iteration per block, blocks issued in element order (as k_inc_fill:
 // the live destination segments stay in L2 until their sectors are complete).
 template <int U>
-__global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, const int32_t* __restrict__ elems,
-                        const int32_t* __restrict__ lab, int32_t* __restrict__ cursor,
-                        uint32_t* __restrict__ linc, int32_t* __restrict__ lel) {
+__global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1,
+                        const int32_t* __restrict__ elems, const int32_t* __restrict__ lab,
+                        int32_t* __restrict__ cursor, uint32_t* __restrict__ linc, int32_t* __restrict__ lel) {
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1;
+    const bool sharded = c0 > 0 || c1 < n_nodes;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t e0 = warp * 32 * U; e0 < n_entries; e0 += nwarps * 32 * U) {
@@ -279,8 +285,23 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, const int32_
             key[u] = -1;
             if (e < n_entries) {
                 const int32_t v = __ldg(elems + e);
-                if ((uint32_t)v < (uint32_t)n_nodes) key[u] = __ldg(lab + v);
-                lel[e] = key[u];
+                // a shard skips the elements that touch none of its columns: no
+                // label gather, no lel row (the column pass never reads it)
+                bool touched = true;
+                if (sharded) {
+                    const int64_t t0 = (int64_t)entry_elem(e, nv) * nv;
+                    touched = false;
+                    for (int i = 0; i < nv; ++i) {
+                        const int32_t w = __ldg(elems + t0 + i);
+                        touched = touched || (w >= c0 && w < c1);
+                    }
+                }
+                if (touched) {
+                    int32_t lb = -1;
+                    if ((uint32_t)v < (uint32_t)n_nodes) lb = __ldg(lab + v);
+                    lel[e] = lb;
+                    if (v >= c0 && v < c1) key[u] = lb;  // keys for this shard's columns only
+                }
             }
         }
 #pragma unroll
@@ -295,109 +316,11 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, const int32_
             const int32_t p0 = __shfl_sync(kFull, pos[u], __ffs(grp[u]) - 1) + __popc(grp[u] & lower);
             if (key[u] >= 0) {
                 const int64_t e = e0 + u * 32 + lane;
-                const int32_t t = (int32_t)(e / nv);
+                const int32_t t = entry_elem(e, nv);
                 const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
                 linc[p0] = (j << 30) | (uint32_t)t;
             }
         }
-    }
-}
-
-// ---- block-sorted fill (FL_PLAN=s; measured SLOWER than the direct fill on C5,
-// 5.58 vs 3.64 ms: the shared-memory hash, its scan and 40 KB of shared memory
-// per block cost more than the scattered stores it saves).  A block takes
-// 2048 consecutive entries; their labels repeat ~6 times (a node's incident
-// elements are neighbours in the element stream), so the block groups its
-// entries by label in shared memory (hash of labels), reserves each label's run
-// with ONE global atomic, and writes the keys out in label order: consecutive
-// threads store consecutive slots of a run instead of 32 scattered keys per
-// store instruction.  Slot order inside a run is arbitrary either way (the
-// column kernel sorts its keys).
-constexpr int kSF = 8;                       // entries per thread
-constexpr int kSFChunk = kP4Block * kSF;     // 2048 entries per block
-constexpr int kSFHash = 2048;                // label hash slots (power of 2, >= entries per block)
-
-__global__ void __launch_bounds__(kP4Block)
-k4_fill_sorted(int64_t n_entries, int nv, int32_t n_nodes, const int32_t* __restrict__ elems,
-               const int32_t* __restrict__ lab, int32_t* __restrict__ cursor, uint32_t* __restrict__ linc,
-               int32_t* __restrict__ lel) {
-    __shared__ int32_t hkey[kSFHash];
-    __shared__ int32_t hcnt[kSFHash];  // count, then the run's first sorted position
-    __shared__ int32_t hbase[kSFHash]; // the run's first global slot
-    __shared__ int2 sorted[kSFChunk];  // (global slot, key) in label order
-    __shared__ int32_t wsum[kP4Block / 32];
-    const int tid = threadIdx.x;
-    const int64_t e0 = (int64_t)blockIdx.x * kSFChunk;
-    for (int h = tid; h < kSFHash; h += kP4Block) {
-        hkey[h] = -1;
-        hcnt[h] = 0;
-    }
-    __syncthreads();
-    int32_t slot[kSF], rank[kSF];
-    uint32_t key[kSF];
-#pragma unroll
-    for (int k = 0; k < kSF; ++k) {
-        const int64_t e = e0 + (int64_t)k * kP4Block + tid;
-        slot[k] = -1;
-        if (e < n_entries) {
-            const int32_t v = __ldg(elems + e);
-            const int32_t lb = (uint32_t)v < (uint32_t)n_nodes ? __ldg(lab + v) : -1;
-            lel[e] = lb;
-            if (lb >= 0) {
-                const int32_t t = (int32_t)(e / nv);
-                key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
-                uint32_t h = ((uint32_t)lb * 2654435761u) >> (32 - lg2c(kSFHash));
-                while (true) {  // the table holds <= 2048 labels: always finds a slot
-                    const int32_t old = atomicCAS(&hkey[h], -1, lb);
-                    if (old == -1 || old == lb) break;
-                    h = (h + 1) & (kSFHash - 1);
-                }
-                slot[k] = (int32_t)h;
-                rank[k] = atomicAdd(&hcnt[h], 1);
-            }
-        }
-    }
-    __syncthreads();
-    // runs in slot order: exclusive scan of the counts over the table
-    constexpr int PER = kSFHash / kP4Block;  // slots per thread (contiguous)
-    int32_t c[PER], tot = 0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        c[q] = hcnt[tid * PER + q];
-        tot += c[q];
-    }
-    const int lane = tid & 31, w = tid >> 5;
-    int32_t incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    int32_t before = 0, nsorted = 0;
-    for (int i = 0; i < kP4Block / 32; ++i) {
-        if (i < w) before += wsum[i];
-        nsorted += wsum[i];
-    }
-    int32_t run = before + incl - tot;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int h = tid * PER + q;
-        if (c[q]) {
-            hbase[h] = atomicAdd(cursor + hkey[h], c[q]);  // one reservation per label
-            hcnt[h] = run;
-        }
-        run += c[q];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kSF; ++k)
-        if (slot[k] >= 0) sorted[hcnt[slot[k]] + rank[k]] = make_int2(hbase[slot[k]] + rank[k], (int32_t)key[k]);
-    __syncthreads();
-    for (int q = tid; q < nsorted; q += kP4Block) {
-        const int2 x = sorted[q];
-        linc[x.x] = (uint32_t)x.y;
     }
 }
 
@@ -411,12 +334,14 @@ k4_fill_sorted(int64_t n_entries, int nv, int32_t n_nodes, const int32_t* __rest
 constexpr int kB4Items = 16, kB4MaxBuckets = 1024;
 
 __global__ void __launch_bounds__(kP4Block)
-k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int shift, const int32_t* __restrict__ elems,
-                  const int32_t* __restrict__ lab, const int32_t* __restrict__ lptr, int32_t* __restrict__ bcur,
-                  int2* __restrict__ stage, int32_t* __restrict__ lel) {
+k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1, int shift,
+                  const int32_t* __restrict__ elems, const int32_t* __restrict__ lab,
+                  const int32_t* __restrict__ lptr, int32_t* __restrict__ bcur, int2* __restrict__ stage,
+                  int32_t* __restrict__ lel) {
     __shared__ int32_t hist[kB4MaxBuckets];
     __shared__ int32_t base[kB4MaxBuckets];
     const int nb = ((n_nodes - 1) >> shift) + 1;
+    const bool sharded = c0 > 0 || c1 < n_nodes;
     constexpr int CH = kP4Block * kB4Items;
     const int64_t e0 = (int64_t)blockIdx.x * CH;
     for (int b = threadIdx.x; b < nb; b += kP4Block) hist[b] = 0;
@@ -429,10 +354,22 @@ k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int shift, const i
         lv[k] = -1;
         if (e < n_entries) {
             const int32_t v = __ldg(elems + e);
-            if ((uint32_t)v < (uint32_t)n_nodes) lv[k] = __ldg(lab + v);
-            lel[e] = lv[k];
+            bool touched = true;  // a shard skips the elements touching none of its columns
+            if (sharded) {
+                const int64_t t0 = (int64_t)entry_elem(e, nv) * nv;
+                touched = false;
+                for (int i = 0; i < nv; ++i) {
+                    const int32_t w = __ldg(elems + t0 + i);
+                    touched = touched || (w >= c0 && w < c1);
+                }
+            }
+            if (touched) {
+                if ((uint32_t)v < (uint32_t)n_nodes) lv[k] = __ldg(lab + v);
+                lel[e] = lv[k];
+            }
+            if (v < c0 || v >= c1) lv[k] = -1;  // staged for this shard's columns only
             if (lv[k] >= 0) {
-                const int32_t t = (int32_t)(e / nv);
+                const int32_t t = entry_elem(e, nv);
                 key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
                 rk[k] = atomicAdd(&hist[lv[k] >> shift], 1);
             }
@@ -467,13 +404,14 @@ k4_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage, int
 }
 
 // stats[0] += sum_l min(m_l d + 1, N) (nnz upper bound), stats[1] = max m_l
-__global__ void k4_stats(int32_t n, int dim, const int32_t* __restrict__ lptr, P4Misc* __restrict__ misc) {
+__global__ void k4_stats(int32_t n, int32_t n_rows, int dim, const int32_t* __restrict__ lptr,
+                         P4Misc* __restrict__ misc) {
     int64_t bound = 0;
     int32_t mx = 0;
     for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
         const int32_t m = lptr[c + 1] - lptr[c];
         const int64_t b = (int64_t)m * dim + 1;
-        bound += b < n ? b : n;
+        bound += b < n_rows ? b : n_rows;
         mx = m > mx ? m : mx;
     }
 #pragma unroll
@@ -1127,7 +1065,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                     u0 = fc_c < 0 ? node_field4(p.g_dir, p.nodes, D, c) : 0.0;
                     bmod = LIFT ? b - ylift : b - 0.0;  // system.hpp:197-198
                 }
-                p.vst[c] = make_double4(b, u0, bmod, __longlong_as_double((long long)meta));
+                p.vst[c - p.c_begin] = make_double4(b, u0, bmod, __longlong_as_double((long long)meta));
             }
             __syncwarp();
         }
@@ -1156,9 +1094,12 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
-    const int32_t v = (int32_t)(tile * kPlaceThreads) + threadIdx.x;
+    const int32_t v = (int32_t)(tile * kPlaceThreads) + threadIdx.x;  // column c_begin + v
     const bool in = v < N;
-    const int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + v) : -1;
+    // free ranks relative to the shard: free nodes below c_begin come first
+    const int32_t fb = p.want_sys ? free_base(p) : 0;
+    int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + p.c_begin + v) : -1;
+    if (fr >= 0) fr -= fb;
     double4 vs = make_double4(0.0, 0.0, 0.0, 0.0);
     if (in) vs = ld_xl(p.vst + v);  // the record of node v, in node order
     const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
@@ -1189,7 +1130,8 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
         if (fr >= 0) p.ff_col_ptr[fr] = pf;
         if (v == N - 1) {
             p.col_ptr[N] = pa + ca;
-            if (p.want_sys) p.ff_col_ptr[__ldg(p.fidx + 2 * (int64_t)N + 1)] = pf + cf;
+            if (p.want_sys)  // free_rank[c_begin + N] - free_rank[c_begin] free columns
+                p.ff_col_ptr[__ldg(p.fidx + (int64_t)p.n_nodes + 1 + p.c_begin + N) - fb] = pf + cf;
         }
         if ((int64_t)pa + ca > p.cap_a || (p.want_sys && (int64_t)pf + cf > p.cap_ff)) atomicOr(p.err, DERR_CAPACITY);
     }
@@ -1259,6 +1201,9 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     auto& lp = mesh->lp;
     const int nv = mesh->dim + 1;
     const int32_t N = mesh->n_nodes;
+    // owned columns (a multi-GPU shard); the whole mesh otherwise
+    const int32_t c0 = mesh->col_begin, c1 = mesh->col_end;
+    const bool sharded = c0 != 0 || c1 != N;
     const int64_t n_entries = (int64_t)mesh->n_elems * nv;
     FL_TRY(lp.lab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.ilab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
@@ -1276,7 +1221,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
     const int64_t cblocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
     const char* lenv = std::getenv("FL_LABELS");
-    if (lenv && lenv[0] == 'f') {
+    if (lenv && lenv[0] == 'f' && !sharded) {
         // first touch in element order (no coordinates involved)
         if (n_entries > 0) {
             k4_count<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, lab, ilab, misc);
@@ -1294,7 +1239,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         const int64_t cn = cenv ? std::max(1, std::atoi(cenv)) : 8;
         int bits = 1;
         while (bits < (dim == 3 ? 10 : 15) && ((int64_t)1 << (dim * (bits + 1))) * cn <= (int64_t)N) ++bits;
-        const int64_t ncell = (int64_t)1 << (dim * bits);
+        const int64_t ncell = ((int64_t)1 << (dim * bits)) * (sharded ? 2 : 1);
         const int nparts = std::min(div_up(N, 256), ctx->sm_count * 4);
         FL_TRY(lp.cells.ensure(sizeof(int32_t) * ((size_t)N + 2 * (size_t)ncell + 2) + sizeof(double) * (6 * (size_t)nparts + 1)));
         int32_t* cellv = lp.cells.as<int32_t>();
@@ -1305,7 +1250,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         k4_bbox<<<nparts, 256, 0, s>>>(N, dim, mesh->nodes.as<double>(), part);
         count_launch(ctx);
         k4_cell<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, dim, bits, nparts, mesh->nodes.as<double>(),
-                                                                          part, cellv, ccnt);
+                                                                          part, c0, c1, cellv, ccnt);
         count_launch(ctx);
         FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(std::max<int64_t>(N, ncell))));
         const int32_t* cc = ccnt;
@@ -1315,7 +1260,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         k4_cell_scatter<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, cellv, coff, lab, ilab);
         count_launch(ctx);
         if (n_entries > 0) {
-            k4_count_plain<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, misc);
+            k4_count_plain<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, c0, c1, mesh->elems.as<int32_t>(), cnt, misc);
             count_launch(ctx);
         }
     }
@@ -1341,28 +1286,23 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         int32_t* bcur = reinterpret_cast<int32_t*>(stg + n_entries);
         FL_CUDA(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (size_t)(nb + 1), s));
         const int64_t chunks = (n_entries + kP4Block * kB4Items - 1) / (kP4Block * kB4Items);
-        k4_bucket_scatter<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, shift, mesh->elems.as<int32_t>(), lab,
-                                                           lp.lptr.as<int32_t>(), bcur, stg, lp.lel.as<int32_t>());
+        k4_bucket_scatter<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, c0, c1, shift, mesh->elems.as<int32_t>(),
+                                                           lab, lp.lptr.as<int32_t>(), bcur, stg,
+                                                           lp.lel.as<int32_t>());
         count_launch(ctx);
         const int bgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, kP4Block * 4), 1), INT_MAX);
         k4_fill_b<<<bgrid, kP4Block, 0, s>>>(lp.lptr.as<int32_t>() + N, stg, cnt, lp.linc.as<uint32_t>());
         count_launch(ctx);
-    } else if (n_entries > 0 && penv && penv[0] == 's') {
-        // FL_PLAN=s: block-sorted fill (measured slower on C5: 5.58 vs 3.64 ms)
-        const int64_t chunks = (n_entries + kSFChunk - 1) / kSFChunk;
-        k4_fill_sorted<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, mesh->elems.as<int32_t>(), lab, cnt,
-                                                        lp.linc.as<uint32_t>(), lp.lel.as<int32_t>());
-        count_launch(ctx);
     } else if (n_entries > 0) {  // the direct fill (one key per store)
         constexpr int U = 4;
         const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
-        k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, mesh->elems.as<int32_t>(), lab, cnt,
+        k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, c0, c1, mesh->elems.as<int32_t>(), lab, cnt,
                                          lp.linc.as<uint32_t>(), lp.lel.as<int32_t>());
         count_launch(ctx);
     }
-    if (N > 0) {
-        k4_stats<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, mesh->dim, lp.lptr.as<int32_t>(),
-                                                                            misc);
+    if (c1 > c0) {  // statistics over the owned labels [0, c1 - c0)
+        k4_stats<<<std::min(div_up(c1 - c0, 256), ctx->sm_count * 8), 256, 0, s>>>(c1 - c0, N, mesh->dim,
+                                                                                  lp.lptr.as<int32_t>(), misc);
         count_launch(ctx);
     }
     FL_CUDA(cudaGetLastError());
@@ -1414,8 +1354,8 @@ static int launch4_sel(fl_ctx* ctx, ColParams& p) {
     }
 }
 
-// The column pass of fl_assemble on the label plan (whole mesh, no Neumann data:
-// fl_api.cu routes those to the id-space kernels).  p carries the outputs, the
+// The column pass of fl_assemble on the label plan (the whole mesh or a column
+// range; meshes with Neumann data are routed to the id-space kernels by fl_api.cu).  p carries the outputs, the
 // fields and the partition; the plan pointers are replaced here by the label plan's.
 int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     const cudaStream_t s = ctx->stream;
@@ -1462,8 +1402,8 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     }
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], s));
     // placement: column pointers in node-id order, the copy and the vectors, one pass
-    if (N > 0) {
-        const int64_t ptiles = ((int64_t)N + kPlaceThreads - 1) / kPlaceThreads;
+    if (p.n_cols > 0) {
+        const int64_t ptiles = ((int64_t)p.n_cols + kPlaceThreads - 1) / kPlaceThreads;
         FL_TRY(res->v4[2].ensure(sizeof(uint64_t) * (size_t)(ptiles + 2)));
         uint64_t* status = res->v4[2].as<uint64_t>();
         FL_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)(ptiles + 2), s));

@@ -97,7 +97,7 @@ __global__ void k_inc_fill(int32_t n_elems, int nv, int32_t n_nodes, int32_t c_b
             const int32_t p0 = __shfl_sync(0xffffffffu, pos[u], __ffs(grp[u]) - 1) + __popc(grp[u] & lower);
             if (key[u] >= 0) {
                 const int64_t e = e0 + u * 32 + lane;
-                const int32_t t = (int32_t)(e / nv);
+                const int32_t t = entry_elem(e, nv);
                 const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
                 inc[p0] = (j << 30) | (uint32_t)t;
                 if (emark) emark[t] = 1;
@@ -163,7 +163,7 @@ k_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c_begin, in
                 const uint32_t l = (uint32_t)(v - c_begin);
                 if (v >= 0 && v < n_nodes && l < (uint32_t)n_cols) {
                     lv[k] = (int32_t)l;
-                    const int32_t t = (int32_t)(e / nv);
+                    const int32_t t = entry_elem(e, nv);
                     key[k] = ((uint32_t)(e - (int64_t)t * nv) << 30) | (uint32_t)t;
                     rk[k] = atomicAdd(&hist[l >> shift], 1);
                 }

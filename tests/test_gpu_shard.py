@@ -4,7 +4,8 @@ column-sharded (multi-GPU) path against the unsharded one.
 Sharding runs every rank's column range on the one GPU in turn (no rank waits
 on another: the ranks are independent by construction); the
 stitched shards must equal the reference's single CSC bit for bit, for each
-column kernel (FL_KERNEL=1 general, 2 tiled, 3 register-centric).
+column kernel (FL_KERNEL=0 the default label-space pipeline, 1 general, 2 tiled,
+3 register-centric).
 """
 from __future__ import annotations
 
@@ -70,7 +71,7 @@ def _shards(m, world, what, ctx, **fields):
     return out
 
 
-@pytest.mark.parametrize("kernel", ["1", "2", "3"])
+@pytest.mark.parametrize("kernel", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
 @pytest.mark.parametrize("tag", ["square8_jit", "cube3_mixed_jit", "lshape4_jit"])
 def test_sharded_stiffness_and_load(tag, world, kernel, ctx, monkeypatch):
@@ -110,6 +111,42 @@ def test_sharded_system(tag, gspec, world, ctx):
         assert _bits(got) == _bits(full), which
     for _, r, _ in parts:  # the partition outputs stay global
         np.testing.assert_array_equal(r.partition().free_nodes, ref.partition.free_nodes)
+
+
+@pytest.mark.parametrize("world", [2, 4, 7])
+@pytest.mark.parametrize("name,n", [("C5", 12), ("C3", 48)])
+def test_sharded_label_pipeline_permuted(name, n, world, ctx, ref_which):
+    """Random node ids (the C3 / C5 recipes at small n): every shard's columns are
+    scattered over the domain; the label-space pipeline orders the owned nodes
+    first.  Stitched A, A(free, free) and vectors against the reference, and the
+    asynchronous re-plan (FL_REPLAN) on a range set earlier."""
+    from paper_1804_05156_b200 import configs
+    cfg = configs.build(name, n=n, f_mode="samples")
+    m = cfg.mesh
+    coef = configs.host_samples(m, rule=1, kind=7) if cfg.coef else None
+    a = po.assemble_blockwise(m.dim, m.nodes, m.elems, coef=coef, which=ref_which)
+    ref = fl.poisson_system(m, cfg.f, "x", coef=coef, ctx=ctx)
+    fields = dict(f=cfg.f, g_dirichlet="x", coef=coef)
+    first, second, keep = [], [], []
+    for r in range(world):
+        sa = ShardedAssembler(m, r, world, ctx=ctx)
+        keep.append(sa)  # the device mesh outlives its results' fl_result_sizes
+        first.append(sa.assemble(_lib.OUT_SYSTEM, **fields))
+        # the same range again, re-planned asynchronously with the first plan's bounds
+        second.append(sa.assemble(_lib.OUT_SYSTEM | _lib.REPLAN, **fields))
+    for parts in (first, second):
+        full = stitch_csc(m.num_nodes(), [(r.matrix().col_ptr, r.matrix().row_idx, r.matrix().values)
+                                          for r in parts])
+        np.testing.assert_array_equal(full.col_ptr, a.col_ptr)
+        np.testing.assert_array_equal(full.row_idx, a.row_idx)
+        assert _bits(full.values) == _bits(a.values)
+        aff = stitch_csc(ref.a_ff.m, [(r.matrix_ff().col_ptr, r.matrix_ff().row_idx,
+                                       r.matrix_ff().values) for r in parts])
+        np.testing.assert_array_equal(aff.col_ptr, ref.a_ff.col_ptr)
+        np.testing.assert_array_equal(aff.row_idx, ref.a_ff.row_idx)
+        assert _bits(aff.values) == _bits(ref.a_ff.values)
+        for which, want in [(_lib.U0, ref.u0), (_lib.B_MOD, ref.b_mod), (_lib.B_F, ref.b_f), (_lib.B, ref.b)]:
+            assert _bits(np.concatenate([r.vector(which) for r in parts])) == _bits(want), which
 
 
 def test_set_columns_rejects_bad_range(ctx):
