@@ -710,6 +710,8 @@ FL_API int fl_result_sizes(fl_result* res, fl_sizes* out) {
             lm->lp.stale = false;
             replanned = true;
             if ((uint32_t)(h4[4] >> 32) & DERR_INDEX) h[CNT_ERR] |= DERR_INDEX;
+            // the bucketed fill dropped entries of an over-full bucket
+            if ((uint32_t)(h4[4] >> 32) & DERR_V2_OVERFLOW) h[CNT_ERR] |= DERR_V2_OVERFLOW;
         }
         if (lm && lm->stats_stale && !res->v4_used) {  // an asynchronous re-plan ran with the old bounds
             lm->nnz_bound = (int64_t)hst[0];

@@ -240,41 +240,24 @@ __global__ void k4_cell_scatter(int32_t n, const int32_t* __restrict__ cell, int
     }
 }
 
-// incidence counts per node (label-free count pass of the spatial labelling)
-__global__ void __launch_bounds__(kP4Block)
-k4_count_plain(int64_t n_entries, int32_t n_nodes, int32_t c0, int32_t c1, const int32_t* __restrict__ elems,
-               int32_t* __restrict__ cnt, P4Misc* __restrict__ misc) {
-    const unsigned lower = (1u << (threadIdx.x & 31)) - 1;
-    const int64_t b0 = (int64_t)blockIdx.x * kP4Block * kP4Iters;
-    uint32_t err = 0;
-    for (int k = 0; k < kP4Iters; ++k) {
-        const int64_t e = b0 + (int64_t)k * kP4Block + threadIdx.x;
-        if (e - (threadIdx.x & 31) >= n_entries) break;  // warp-uniform
-        int32_t key = -1;
-        if (e < n_entries) {
-            const int32_t v = __ldg(elems + e);
-            if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
-            else if (v >= c0 && v < c1) key = v;  // columns of this shard
-        }
-        const unsigned g = __match_any_sync(kFull, key);
-        if (key >= 0 && (g & lower) == 0) atomicAdd(cnt + key, __popc(g));
-    }
-    if (__any_sync(kFull, err != 0) && (threadIdx.x & 31) == 0) atomicOr(&misc->err, DERR_INDEX);
-}
-
-// (j << 30 | t) keys into the label segments (cursor seeded with lptr) and the
-// elements with vertex labels.  U rounds of 32 consecutive entries per warp,
-// one warp iteration per block, blocks issued in element order (as k_inc_fill:
-// the live destination segments stay in L2 until their sectors are complete).
+// (j << 30 | t) keys into the label segments and the elements with vertex labels
+// (lel), one pass: label l owns the `cap` slots linc[l * cap ..], its count
+// cnt[l] (zeroed before) is the fill cursor -- no separate count pass, no scan.
+// Slots beyond cap are dropped; the count keeps running, so a valence above cap
+// shows in the statistics and in the column kernel (which then defers to the
+// general kernel).  U rounds of 32 consecutive entries per warp, blocks issued in
+// element order (the live segments stay in L2 until their sectors are complete).
 template <int U>
-__global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1,
+__global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1, int cap,
                         const int32_t* __restrict__ elems, const int32_t* __restrict__ lab,
-                        int32_t* __restrict__ cursor, uint32_t* __restrict__ linc, int32_t* __restrict__ lel) {
+                        int32_t* __restrict__ cnt, uint32_t* __restrict__ linc, int32_t* __restrict__ lel,
+                        P4Misc* __restrict__ misc) {
     const int lane = threadIdx.x & 31;
     const unsigned lower = (1u << lane) - 1;
     const bool sharded = c0 > 0 || c1 < n_nodes;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t err = 0;
     for (int64_t e0 = warp * 32 * U; e0 < n_entries; e0 += nwarps * 32 * U) {
         int32_t key[U];
         unsigned grp[U];
@@ -296,6 +279,7 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
                         touched = touched || (w >= c0 && w < c1);
                     }
                 }
+                if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
                 if (touched) {
                     int32_t lb = -1;
                     if ((uint32_t)v < (uint32_t)n_nodes) lb = __ldg(lab + v);
@@ -309,19 +293,20 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             pos[u] = 0;
-            if (key[u] >= 0 && (grp[u] & lower) == 0) pos[u] = atomicAdd(cursor + key[u], __popc(grp[u]));
+            if (key[u] >= 0 && (grp[u] & lower) == 0) pos[u] = atomicAdd(cnt + key[u], __popc(grp[u]));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t p0 = __shfl_sync(kFull, pos[u], __ffs(grp[u]) - 1) + __popc(grp[u] & lower);
-            if (key[u] >= 0) {
+            if (key[u] >= 0 && p0 < cap) {
                 const int64_t e = e0 + u * 32 + lane;
                 const int32_t t = entry_elem(e, nv);
                 const uint32_t j = (uint32_t)(e - (int64_t)t * nv);
-                linc[p0] = (j << 30) | (uint32_t)t;
+                linc[(int64_t)key[u] * cap + p0] = (j << 30) | (uint32_t)t;
             }
         }
     }
+    if (__any_sync(kFull, err != 0) && lane == 0) atomicOr(&misc->err, DERR_INDEX);
 }
 
 // ---- bucketed fill (large 2-D meshes, element order not spatial: C3).  The
@@ -329,15 +314,16 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
 // sector read-modify-write.  Instead: (1) partition (label, key) pairs into
 // buckets of 2^shift consecutive labels (block-local shared-memory ranks, one
 // global reservation per bucket per block: coalesced runs), writing lel on the
-// way; (2) fill from the staging in bucket order, so the live range of the
+// way; bucket b's staging area is its labels' capacity, (b << shift) * cap on;
+// (2) fill from the staging in bucket order, so the live range of the
 // incidence array is one bucket's slice, resident in L2.
 constexpr int kB4Items = 16, kB4MaxBuckets = 1024;
 
 __global__ void __launch_bounds__(kP4Block)
-k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1, int shift,
+k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_t c1, int shift, int cap,
                   const int32_t* __restrict__ elems, const int32_t* __restrict__ lab,
-                  const int32_t* __restrict__ lptr, int32_t* __restrict__ bcur, int2* __restrict__ stage,
-                  int32_t* __restrict__ lel) {
+                  int32_t* __restrict__ bcur, int2* __restrict__ stage, int32_t* __restrict__ lel,
+                  P4Misc* __restrict__ misc) {
     __shared__ int32_t hist[kB4MaxBuckets];
     __shared__ int32_t base[kB4MaxBuckets];
     const int nb = ((n_nodes - 1) >> shift) + 1;
@@ -348,6 +334,7 @@ k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_
     __syncthreads();
     int32_t lv[kB4Items], rk[kB4Items];
     uint32_t key[kB4Items];
+    uint32_t err = 0;
 #pragma unroll
     for (int k = 0; k < kB4Items; ++k) {
         const int64_t e = e0 + k * kP4Block + threadIdx.x;
@@ -363,6 +350,7 @@ k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_
                     touched = touched || (w >= c0 && w < c1);
                 }
             }
+            if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
             if (touched) {
                 if ((uint32_t)v < (uint32_t)n_nodes) lv[k] = __ldg(lab + v);
                 lel[e] = lv[k];
@@ -375,41 +363,51 @@ k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_
             }
         }
     }
+    if (err) atomicOr(&misc->err, DERR_INDEX);
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += kP4Block)
-        if (hist[b]) base[b] = __ldg(lptr + min((int64_t)b << shift, (int64_t)n_nodes)) + atomicAdd(bcur + b, hist[b]);
+        if (hist[b]) base[b] = atomicAdd(bcur + b, hist[b]);
     __syncthreads();
+    const int32_t bucket_cap = cap << shift;
 #pragma unroll
     for (int k = 0; k < kB4Items; ++k)
-        if (lv[k] >= 0) stage[base[lv[k] >> shift] + rk[k]] = make_int2(lv[k], (int32_t)key[k]);
+        if (lv[k] >= 0) {
+            const int b = lv[k] >> shift;
+            const int32_t q = base[b] + rk[k];
+            if (q < bucket_cap) stage[(int64_t)b * bucket_cap + q] = make_int2(lv[k], (int32_t)key[k]);
+            else atomicOr(&misc->err, DERR_V2_OVERFLOW);  // some label of the bucket exceeds cap
+        }
 }
 
-// staged incidences in bucket order -> their label segments (total = lptr[N])
+// staged incidences in bucket order -> their label segments.  Block = (bucket,
+// chunk of 4 * 256 staged entries); chunks past the bucket's count exit.
 __global__ void __launch_bounds__(kP4Block)
-k4_fill_b(const int32_t* __restrict__ total, const int2* __restrict__ stage, int32_t* __restrict__ cursor,
-          uint32_t* __restrict__ linc) {
-    const int64_t n_staged = *total;
-    for (int64_t q0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; q0 < n_staged;
-         q0 += (int64_t)gridDim.x * blockDim.x * 4) {
-        int2 sv[4];
-        int32_t pos[4];
+k4_fill_b(int shift, int cap, int chunks_per_bucket, const int32_t* __restrict__ bcur,
+          const int2* __restrict__ stage, int32_t* __restrict__ cnt, uint32_t* __restrict__ linc) {
+    const int b = blockIdx.x / chunks_per_bucket, ch = blockIdx.x - b * chunks_per_bucket;
+    const int32_t bucket_cap = cap << shift;
+    const int32_t n_staged = min(__ldg(bcur + b), bucket_cap);
+    const int32_t q0 = (ch * kP4Block + threadIdx.x) * 4;
+    if (q0 >= n_staged) return;
+    const int2* st = stage + (int64_t)b * bucket_cap;
+    int2 sv[4];
+    int32_t pos[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) sv[u] = q0 + u < n_staged ? __ldg(stage + q0 + u) : make_int2(-1, 0);
+    for (int u = 0; u < 4; ++u) sv[u] = q0 + u < n_staged ? __ldg(st + q0 + u) : make_int2(-1, 0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) pos[u] = sv[u].x >= 0 ? atomicAdd(cursor + sv[u].x, 1) : 0;
+    for (int u = 0; u < 4; ++u) pos[u] = sv[u].x >= 0 ? atomicAdd(cnt + sv[u].x, 1) : 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (sv[u].x >= 0) linc[pos[u]] = (uint32_t)sv[u].y;
-    }
+    for (int u = 0; u < 4; ++u)
+        if (sv[u].x >= 0 && pos[u] < cap) linc[(int64_t)sv[u].x * cap + pos[u]] = (uint32_t)sv[u].y;
 }
 
 // stats[0] += sum_l min(m_l d + 1, N) (nnz upper bound), stats[1] = max m_l
-__global__ void k4_stats(int32_t n, int32_t n_rows, int dim, const int32_t* __restrict__ lptr,
+__global__ void k4_stats(int32_t n, int32_t n_rows, int dim, const int32_t* __restrict__ lcnt,
                          P4Misc* __restrict__ misc) {
     int64_t bound = 0;
     int32_t mx = 0;
     for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-        const int32_t m = lptr[c + 1] - lptr[c];
+        const int32_t m = lcnt[c];
         const int64_t b = (int64_t)m * dim + 1;
         bound += b < n_rows ? b : n_rows;
         mx = m > mx ? m : mx;
@@ -625,15 +623,15 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
         bool bad = false;
         const int32_t lc0 = (int32_t)(tile * C::WTC);
         const int ncol_t = (int)min((int64_t)C::WTC, (int64_t)p.n_cols - lc0);
-        const int32_t ipl = lane <= ncol_t ? __ldg(p.inc_ptr + lc0 + lane) : 0;
-        const int32_t ipe = __ldg(p.inc_ptr + lc0 + ncol_t);
-        auto col_range = [&](int q, int32_t& p0, int32_t& m) {
-            const int32_t a = __shfl_sync(kFull, ipl, q & 31);
-            const int32_t b = __shfl_sync(kFull, ipl, (q + 1) & 31);
-            p0 = a;
-            m = q < ncol_t ? ((q + 1 >= ncol_t) ? ipe : b) - a : 0;
+        // label l's keys are the first lcnt[l] of the lcap slots at inc[l * lcap]
+        const int32_t mcl = lane < ncol_t ? __ldg(p.lcnt + lc0 + lane) : 0;
+        auto col_range = [&](int q, int64_t& p0, int32_t& m) {
+            m = __shfl_sync(kFull, mcl, q & 31);
+            if (q >= ncol_t) m = 0;
+            p0 = (int64_t)(lc0 + q) * p.lcap;
         };
-        int32_t p0n, mn;
+        int64_t p0n;
+        int32_t mn;
         col_range(gi, p0n, mn);
         uint32_t key_next[K];
 #pragma unroll
@@ -1205,6 +1203,62 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
 // ===========================================================================
 int v4_lanes(int dim) { return dim == 2 ? 16 : 32; }  // incidences per column the kernel takes
 
+// slots per label segment for a mesh of maximum valence max_inc: the column
+// kernel variant's incidences per column (2-D: 8 lanes x 1 or 2; 3-D: 8 x 4)
+int v4_cap(int dim, int max_inc) { return dim == 2 ? (max_inc <= 8 ? 8 : 16) : 32; }
+
+// keys + relabelled elements for capacity `cap`, then the statistics
+static int v4_fill(fl_ctx* ctx, fl_mesh* mesh, int cap) {
+    const cudaStream_t s = ctx->stream;
+    auto& lp = mesh->lp;
+    const int nv = mesh->dim + 1;
+    const int32_t N = mesh->n_nodes;
+    const int32_t c0 = mesh->col_begin, c1 = mesh->col_end;
+    const int64_t n_entries = (int64_t)mesh->n_elems * nv;
+    P4Misc* misc = lp.misc.as<P4Misc>();
+    int32_t* cnt = lp.lptr.as<int32_t>();  // per-label counts = fill cursors
+    FL_TRY(lp.linc.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>((int64_t)N * cap, 1)));
+    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
+    // bucketed fill for large 2-D meshes (FL_PLAN=0|1 overrides; the element order
+    // of a 3-D mesh is left spatial by every generator here, C5 included)
+    const char* penv = std::getenv("FL_PLAN");
+    const bool bucketed = n_entries > 0 &&
+                          (penv ? penv[0] == '1' : (mesh->dim == 2 && n_entries >= ((int64_t)1 << 26)));
+    if (bucketed) {
+        int shift = 0;
+        while (((int64_t)(N - 1) >> shift) + 1 > kB4MaxBuckets) ++shift;
+        const int nb = ((N - 1) >> shift) + 1;
+        const int64_t bucket_cap = (int64_t)cap << shift;
+        FL_TRY(lp.stage.ensure(sizeof(int2) * (size_t)(bucket_cap * nb) + sizeof(int32_t) * (kB4MaxBuckets + 1)));
+        int2* stg = lp.stage.as<int2>();
+        int32_t* bcur = reinterpret_cast<int32_t*>(stg + bucket_cap * nb);
+        FL_CUDA(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (size_t)(nb + 1), s));
+        const int64_t chunks = (n_entries + kP4Block * kB4Items - 1) / (kP4Block * kB4Items);
+        k4_bucket_scatter<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, c0, c1, shift, cap,
+                                                           mesh->elems.as<int32_t>(), lp.lab.as<int32_t>(), bcur,
+                                                           stg, lp.lel.as<int32_t>(), misc);
+        count_launch(ctx);
+        const int cpb = (int)((bucket_cap + kP4Block * 4 - 1) / (kP4Block * 4));
+        k4_fill_b<<<nb * cpb, kP4Block, 0, s>>>(shift, cap, cpb, bcur, stg, cnt, lp.linc.as<uint32_t>());
+        count_launch(ctx);
+    } else if (n_entries > 0) {  // the direct fill (one key per store)
+        constexpr int U = 4;
+        const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
+        k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, c0, c1, cap, mesh->elems.as<int32_t>(),
+                                         lp.lab.as<int32_t>(), cnt, lp.linc.as<uint32_t>(), lp.lel.as<int32_t>(),
+                                         misc);
+        count_launch(ctx);
+    }
+    if (c1 > c0) {  // statistics over the owned labels [0, c1 - c0)
+        k4_stats<<<std::min(div_up(c1 - c0, 256), ctx->sm_count * 8), 256, 0, s>>>(c1 - c0, N, mesh->dim, cnt, misc);
+        count_launch(ctx);
+    }
+    FL_CUDA(cudaGetLastError());
+    lp.cap = cap;
+    return FL_OK;
+}
+
 int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     const cudaStream_t s = ctx->stream;
     auto& lp = mesh->lp;
@@ -1217,21 +1271,20 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     FL_TRY(lp.lab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.ilab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.lptr.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-    FL_TRY(lp.lcnt.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-    FL_TRY(lp.linc.ensure(sizeof(uint32_t) * (size_t)std::max<int64_t>(n_entries, 1)));
     FL_TRY(lp.lel.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(n_entries, 4)));
     FL_TRY(lp.misc.ensure(sizeof(P4Misc)));
-    FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(N)));
     P4Misc* misc = lp.misc.as<P4Misc>();
-    int32_t* cnt = lp.lcnt.as<int32_t>();
     int32_t* lab = lp.lab.as<int32_t>();
     int32_t* ilab = lp.ilab.as<int32_t>();
-    FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
-    FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
-    const int64_t cblocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
     const char* lenv = std::getenv("FL_LABELS");
     if (lenv && lenv[0] == 'f' && !sharded) {
-        // first touch in element order (no coordinates involved)
+        // first touch in element order (no coordinates involved; its per-node
+        // counts only detect the first toucher)
+        FL_TRY(lp.lcnt.ensure(sizeof(int32_t) * ((size_t)N + 1)));
+        int32_t* cnt = lp.lcnt.as<int32_t>();
+        FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+        FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
+        const int64_t cblocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
         if (n_entries > 0) {
             k4_count<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, lab, ilab, misc);
             count_launch(ctx);
@@ -1261,60 +1314,20 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         k4_cell<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, dim, bits, nparts, mesh->nodes.as<double>(),
                                                                           part, c0, c1, cellv, ccnt);
         count_launch(ctx);
-        FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(std::max<int64_t>(N, ncell))));
+        FL_TRY(ctx->scan_ws.ensure(scan_ws_bytes(ncell)));
         const int32_t* cc = ccnt;
         FL_CUDA(launch_scan<int32_t>(ncell, [cc] __device__(int64_t i) { return (int64_t)cc[i]; }, coff,
                                      ctx->scan_ws.p, s));
         count_launch(ctx);
         k4_cell_scatter<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, cellv, coff, lab, ilab);
         count_launch(ctx);
-        if (n_entries > 0) {
-            k4_count_plain<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, c0, c1, mesh->elems.as<int32_t>(), cnt, misc);
-            count_launch(ctx);
-        }
     }
-    const int32_t* cc = cnt;
-    const int32_t* il = ilab;
-    FL_CUDA(launch_scan<int32_t>(
-        N, [cc, il] __device__(int64_t i) { return (int64_t)cc[il[i]]; }, lp.lptr.as<int32_t>(),
-        ctx->scan_ws.p, s));
-    count_launch(ctx);
-    // fill cursors start at the segment offsets
-    FL_CUDA(cudaMemcpyAsync(cnt, lp.lptr.p, sizeof(int32_t) * ((size_t)N + 1), cudaMemcpyDeviceToDevice, s));
-    // bucketed fill for large 2-D meshes (FL_PLAN=0|1 overrides; the element order
-    // of a 3-D mesh is left spatial by every generator here, C5 included)
-    const char* penv = std::getenv("FL_PLAN");
-    const bool bucketed = n_entries > 0 &&
-                          (penv ? penv[0] == '1' : (mesh->dim == 2 && n_entries >= ((int64_t)1 << 26)));
-    if (bucketed) {
-        int shift = 0;
-        while (((int64_t)(N - 1) >> shift) + 1 > kB4MaxBuckets) ++shift;
-        const int nb = ((N - 1) >> shift) + 1;
-        FL_TRY(lp.stage.ensure(sizeof(int2) * (size_t)n_entries + sizeof(int32_t) * (kB4MaxBuckets + 1)));
-        int2* stg = lp.stage.as<int2>();
-        int32_t* bcur = reinterpret_cast<int32_t*>(stg + n_entries);
-        FL_CUDA(cudaMemsetAsync(bcur, 0, sizeof(int32_t) * (size_t)(nb + 1), s));
-        const int64_t chunks = (n_entries + kP4Block * kB4Items - 1) / (kP4Block * kB4Items);
-        k4_bucket_scatter<<<(int)chunks, kP4Block, 0, s>>>(n_entries, nv, N, c0, c1, shift, mesh->elems.as<int32_t>(),
-                                                           lab, lp.lptr.as<int32_t>(), bcur, stg,
-                                                           lp.lel.as<int32_t>());
-        count_launch(ctx);
-        const int bgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, kP4Block * 4), 1), INT_MAX);
-        k4_fill_b<<<bgrid, kP4Block, 0, s>>>(lp.lptr.as<int32_t>() + N, stg, cnt, lp.linc.as<uint32_t>());
-        count_launch(ctx);
-    } else if (n_entries > 0) {  // the direct fill (one key per store)
-        constexpr int U = 4;
-        const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
-        k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, c0, c1, mesh->elems.as<int32_t>(), lab, cnt,
-                                         lp.linc.as<uint32_t>(), lp.lel.as<int32_t>());
-        count_launch(ctx);
-    }
-    if (c1 > c0) {  // statistics over the owned labels [0, c1 - c0)
-        k4_stats<<<std::min(div_up(c1 - c0, 256), ctx->sm_count * 8), 256, 0, s>>>(c1 - c0, N, mesh->dim,
-                                                                                  lp.lptr.as<int32_t>(), misc);
-        count_launch(ctx);
-    }
-    FL_CUDA(cudaGetLastError());
+    // Segment capacity: a re-plan keeps the last known valence class (a topology
+    // that outgrows it is flagged by the column kernel and rerun on the general
+    // kernel, fl_result_sizes); the first plan fills at the largest class and,
+    // should the mesh fit a smaller one, once more at that.
+    const int lanes = v4_lanes(mesh->dim);
+    FL_TRY(v4_fill(ctx, mesh, sync ? lanes : v4_cap(mesh->dim, lp.max_inc)));
     lp.planned = true;
     lp.ever = true;
     if (!sync) {
@@ -1331,7 +1344,8 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     }
     lp.nnz_bound = (int64_t)h->stats[0];
     lp.max_inc = (int32_t)h->stats[1];
-    lp.ok = lp.max_inc <= v4_lanes(mesh->dim);
+    lp.ok = lp.max_inc <= lanes && !(h->err & DERR_V2_OVERFLOW);
+    if (lp.ok && v4_cap(mesh->dim, lp.max_inc) < lanes) FL_TRY(v4_fill(ctx, mesh, v4_cap(mesh->dim, lp.max_inc)));
     return FL_OK;
 }
 
@@ -1379,7 +1393,9 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     p.xl = xl;
     p.vst = res->v4[1].as<double4>();
     p.lel = lp.lel.as<int32_t>();
-    p.inc_ptr = lp.lptr.as<int32_t>();
+    p.inc_ptr = nullptr;
+    p.lcnt = lp.lptr.as<int32_t>();
+    p.lcap = lp.cap;
     p.inc = lp.linc.as<uint32_t>();
     p.keys_sorted = false;
     if (N > 0) {
@@ -1402,9 +1418,8 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     }
     // 8 lanes per column, 4 columns per warp: 2-D 1 or 2 incidences per lane
     // (valence <= 8 / 16), 3-D 4 (valence <= 32)
-    const int kmax = lp.max_inc;
     if (dim == 2) {
-        if (kmax <= 8) FL_TRY((launch4_sel<2, 8, 1>(ctx, p)));
+        if (lp.cap <= 8) FL_TRY((launch4_sel<2, 8, 1>(ctx, p)));
         else FL_TRY((launch4_sel<2, 8, 2>(ctx, p)));
     } else {
         // FL_V4_SHAPE=16x2: 16 lanes x 2 incidences, 2 columns per warp (experiment)
