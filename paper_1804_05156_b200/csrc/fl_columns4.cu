@@ -698,17 +698,17 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                     for (int i = 0; i < NV; ++i) sm.msk[h][i] = 0u;
                 }
             }
+            // the sorted keys wait in cslot (free until the slots are compacted):
+            // one shared load per incidence instead of a register select chain
+            static_assert(C::HS >= LK, "cslot holds the sorted keys during the incidence loop");
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) sm.cslot[kk * L + g] = (int32_t)key[kk];
             __syncwarp();
             // ---- 2. per incidence: geometry of column j of element t from the
             //      label-ordered nodes, staged; its off-diagonal items' rows inserted
             // the element's vertex labels one incidence ahead: incidence kk+1's
             // load is in flight while incidence kk is processed
-            auto key_at = [&](int kk) -> uint32_t {  // register select, no local memory
-                uint32_t k0 = key[0];
-#pragma unroll
-                for (int q2 = 1; q2 < K; ++q2) k0 = (kk == q2) ? key[q2] : k0;
-                return k0;
-            };
+            auto key_at = [&](int kk) -> uint32_t { return (uint32_t)sm.cslot[kk * L + g]; };
             auto lel_of = [&](int kk) {
                 int4 v = make_int4(0, 0, 0, 0);
                 if (kk * L + g < m) {
@@ -789,14 +789,10 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 // exact-zero items are skipped: x + (+-0) == x for x != 0, a zero
                 // prefix only changes the sign of a zero the next nonzero item
                 // absorbs, and an all-zero entry is dropped anyway (sparse.hpp:105)
-                uint32_t todo = 0;
 #pragma unroll
-                for (int i = 0; i < NV; ++i) todo |= (i != j_ && s[i] != 0.0) ? (1u << i) : 0u;
-#pragma unroll 1
-                for (; todo; todo &= todo - 1) {
-                    const int i = __ffs(todo) - 1;
-                    const int32_t r = i == 0 ? R[0] : i == 1 ? R[1] : (i == 2 || D == 2) ? R[2] : R[D];
-                    const int32_t fr = i == 0 ? FR[0] : i == 1 ? FR[1] : (i == 2 || D == 2) ? FR[2] : FR[D];
+                for (int i = 0; i < NV; ++i) {  // static i: R[i], FR[i] stay in their registers
+                    if (i == j_ || s[i] == 0.0) continue;
+                    const int32_t r = R[i], fr = FR[i];
                     uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - lg2c(C::HS));
                     int slot = -1;
 #pragma unroll 1
