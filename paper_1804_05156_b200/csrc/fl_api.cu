@@ -125,6 +125,8 @@ static int rerun_general(fl_result* res, fl_result_ext* x) {
         if (!mesh->planned || mesh->stats_stale) FL_TRY(fl_mesh_plan(ctx, mesh));
         p.inc_ptr = mesh->inc_ptr.as<int32_t>();
         p.inc = mesh->inc.as<uint32_t>();
+        p.lcnt = nullptr;
+        p.nadd = nullptr;  // the general kernel forms the Neumann shares itself
         res->v4_used = false;
     }
     // the general kernel may need the plan's full output bound
@@ -477,14 +479,11 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     const bool need_plan = what & (FL_OUT_STIFFNESS | FL_OUT_LOAD);
     const char* kern = std::getenv("FL_KERNEL");
     const char kk = kern ? kern[0] : '0';
-    // the label-space pipeline (fl_columns4.cu) takes meshes (whole or a column
-    // range) without Neumann data whose valence fits its kernel; FL_V4=0 forces
-    // the id-space one
+    // the label-space pipeline (fl_columns4.cu) takes every mesh (whole or a
+    // column range) whose valence fits its kernel; FL_V4=0 forces the id-space one
     const char* v4env = std::getenv("FL_V4");
-    const bool neu_data = (what & FL_OUT_LOAD) && mesh->has_flags && g_neumann &&
-                          g_neumann->kind != FL_FIELD_NONE;
     bool use_v4 = need_plan && kk == '0' && !(v4env && v4env[0] == '0') && mesh->n_nodes > 0 &&
-                  mesh->n_elems > 0 && mesh->lp.ok && !neu_data;
+                  mesh->n_elems > 0 && mesh->lp.ok;
     if (use_v4 && (replan || !mesh->lp.planned)) {
         // a re-plan runs asynchronously with the previous bounds (fl_result_sizes
         // refreshes them and reruns on the general kernel if they were exceeded)

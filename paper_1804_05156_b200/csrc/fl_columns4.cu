@@ -827,8 +827,10 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 }
                 if (m & 1) fold = fold + src[m - 1];
             }
-            const double b = __shfl_sync(kFull, fold, 0, L);
+            double b = __shfl_sync(kFull, fold, 0, L);
             const double dg = __shfl_sync(kFull, fold, 1, L);
+            // apply_neumann (system.hpp:123-172): b + the node's accumulated face shares
+            if (p.nadd && act && p.is_neu[c]) b = b + p.nadd[c - p.c_begin];
             double ylift = 0.0;
             uint64_t meta = 0;  // staging: first entry (40 bits) | count of A | count of A(free, free)
             if (p.want_a) {
@@ -1373,8 +1375,7 @@ static int launch4_sel(fl_ctx* ctx, ColParams& p) {
     }
 }
 
-// The column pass of fl_assemble on the label plan (the whole mesh or a column
-// range; meshes with Neumann data are routed to the id-space kernels by fl_api.cu).  p carries the outputs, the
+// The column pass of fl_assemble on the label plan (the whole mesh or a column range).  p carries the outputs, the
 // fields and the partition; the plan pointers are replaced here by the label plan's.
 int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     const cudaStream_t s = ctx->stream;
@@ -1390,6 +1391,7 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     p.vst = res->v4[1].as<double4>();
     p.lel = lp.lel.as<int32_t>();
     p.inc_ptr = nullptr;
+    p.lab = lp.lab.as<int32_t>();
     p.lcnt = lp.lptr.as<int32_t>();
     p.lcap = lp.cap;
     p.inc = lp.linc.as<uint32_t>();
@@ -1407,6 +1409,9 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     p.st_a_row = res->stage[0].as<int32_t>();
     p.st_a_val = nullptr;
     FL_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(uint32_t), s));
+    // Neumann data: per-node face shares first (k_neumann_add on the label plan)
+    p.nadd = nullptr;
+    if (p.want_b && p.has_neumann && p.g_neu.kind != FL_FIELD_NONE) FL_TRY(launch_neumann_add(ctx, dim, p, res));
     if (ctx->profile) {
         FL_CUDA(cudaEventRecord(ctx->ev[5], s));
         FL_CUDA(cudaEventRecord(ctx->ev[6], s));

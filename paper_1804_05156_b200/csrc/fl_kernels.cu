@@ -1423,8 +1423,8 @@ int launch_hybrid(fl_ctx* ctx, int dim, ColParams& p, fl_mesh* mesh, fl_result* 
 // ---------------------------------------------------------------------------
 // Neumann shares for the register kernel (apply_neumann, system.hpp:123-172):
 // add[c] = 0.0 + the shares of the flag-2 faces containing node c in face-major
-// (lf, t) order; the register kernel then forms b[c] + add[c].  Warp per node on
-// a flag-2 face.
+// (lf, t) order; the column kernel (id-space register kernel or the label-space
+// one) then forms b[c] + add[c].  Warp per node on a flag-2 face.
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(kWarps * 32) k_neumann_add(ColParams p, double* __restrict__ add_out) {
@@ -1440,7 +1440,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_neumann_add(ColParams p, double
         if (!p.is_neu[c]) continue;  // warp-uniform
         if (lane == 0) scnt[w] = 0;
         __syncwarp();
-        const int32_t p0 = p.inc_ptr[lc], m = p.inc_ptr[lc + 1] - p0;
+        // the node's incidences: its id-space segment, or (label plan) the first
+        // lcnt[l] of the lcap slots of its label l
+        int64_t p0;
+        int32_t m;
+        if (p.lcnt) {
+            const int32_t l = __ldg(p.lab + c);
+            p0 = (int64_t)l * p.lcap;
+            m = min(__ldg(p.lcnt + l), p.lcap);
+        } else {
+            p0 = p.inc_ptr[lc];
+            m = p.inc_ptr[lc + 1] - (int32_t)p0;
+        }
         for (int base = 0; base < m; base += 32) {
             if (base + lane < m) {
                 const uint32_t key = __ldg(p.inc + p0 + base + lane);

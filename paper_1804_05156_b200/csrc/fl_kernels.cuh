@@ -85,6 +85,7 @@ struct ColParams {
     // node's coordinates and {node id, free rank or -1} in .w; vst[label] =
     // {b, u0, b - A u0, 0}
     const int32_t* lel;
+    const int32_t* lab;   // node id -> label
     const int32_t* lcnt;  // incidences per label; label l's keys at inc[l * lcap ..]
     int32_t lcap;
     const double4* xl;
