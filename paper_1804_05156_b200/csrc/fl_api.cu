@@ -189,6 +189,11 @@ FL_API int fl_create(int device, fl_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     FL_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
+    FL_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+    FL_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    FL_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    const char* ov = std::getenv("FL_OVERLAP");
+    ctx->overlap = !(ov && ov[0] == '0');
     FL_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     const char* prof = std::getenv("FL_PROFILE");
     ctx->profile = prof && prof[0] == '1';
@@ -205,7 +210,14 @@ FL_API int fl_destroy(fl_ctx* ctx) {
     if (!ctx) return FL_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->aux_stream) {
+        cudaStreamSynchronize(ctx->aux_stream);
+        cudaStreamDestroy(ctx->aux_stream);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     ctx->scan_ws.release();
+    ctx->scan_ws_aux.release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->profile)
         for (auto& ev : ctx->ev) cudaEventDestroy(ev);
@@ -484,7 +496,12 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
     const char* v4env = std::getenv("FL_V4");
     bool use_v4 = need_plan && kk == '0' && !(v4env && v4env[0] == '0') && mesh->n_nodes > 0 &&
                   mesh->n_elems > 0 && mesh->lp.ok;
-    if (use_v4 && (replan || !mesh->lp.planned)) {
+    // An asynchronous label re-plan (previous bounds known) is independent of the
+    // partition + FaceLists pass: it is launched after them, which run on the
+    // side stream beside it (below).
+    const bool defer_plan = use_v4 && (replan || !mesh->lp.planned) && mesh->lp.ever && ctx->overlap &&
+                            (what & FL_OUT_PARTITION);
+    if (use_v4 && (replan || !mesh->lp.planned) && !defer_plan) {
         // a re-plan runs asynchronously with the previous bounds (fl_result_sizes
         // refreshes them and reruns on the general kernel if they were exceeded)
         FL_TRY(v4_plan(ctx, mesh, !mesh->lp.ever));
@@ -505,7 +522,7 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         FL_TRY(fl_mesh_plan(ctx, mesh));
         ctx->plan_timed = true;
     }
-    if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
+    if (ctx->profile && !defer_plan) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
     fl_result_ext* x = ext_of(res);
     res->sizes_valid = false;
     res->v4_used = false;
@@ -565,7 +582,24 @@ FL_API int fl_assemble(fl_ctx* ctx, fl_mesh* mesh, const fl_field* f, const fl_f
         FL_TRY(res->arr[FL_AFF_VALUES].ensure(sizeof(double) * cap));
         FL_CUDA(cudaMemsetAsync(res->arr[FL_AFF_COL_PTR].p, 0, sizeof(int32_t), s));
     }
-    if (want_p) {
+    if (defer_plan) {
+        // fork: partition + FaceLists on the side stream (their own scan workspace),
+        // the label plan on the main one; join before the column pass
+        FL_CUDA(cudaEventRecord(ctx->ev_fork, s));
+        FL_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0));
+        ctx->stream = ctx->aux_stream;
+        std::swap(ctx->scan_ws, ctx->scan_ws_aux);
+        int rc = launch_partition(ctx, mesh, res);
+        if (rc == FL_OK) rc = launch_face_lists(ctx, mesh, res);
+        std::swap(ctx->scan_ws, ctx->scan_ws_aux);
+        ctx->stream = s;
+        cudaEventRecord(ctx->ev_join, ctx->aux_stream);
+        if (rc == FL_OK) rc = v4_plan(ctx, mesh, false);
+        cudaStreamWaitEvent(s, ctx->ev_join, 0);  // join (also on failure: the side stream never runs ahead)
+        if (rc != FL_OK) return rc;
+        ctx->plan_timed = true;
+        if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[1], s));
+    } else if (want_p) {
         FL_TRY(launch_partition(ctx, mesh, res));
         FL_TRY(launch_face_lists(ctx, mesh, res));
     }
