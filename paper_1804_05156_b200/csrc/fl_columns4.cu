@@ -463,8 +463,15 @@ struct V4Smem {  // one per column group
     using C = V4<D, L, K>;
     static constexpr int NV = D + 1;
     alignas(16) int32_t row[C::HS];    // slot -> row (node id, -1 empty)
-    alignas(16) int32_t crow[C::HS];   // occupied rows, compacted (-1 padded)
-    int32_t cslot[C::HS];              // their slots
+    // occupied rows, compacted (-1 padded); during the incidence loop the same
+    // words hold each lane's vertex node ids (lr[g * NV + i]) -- read back with a
+    // run-time i instead of a register select chain
+    union alignas(16) {
+        int32_t crow[C::HS];
+        int32_t lr[L * NV > C::HS ? L * NV : C::HS];
+    };
+    int32_t lfr[L * NV];               // ... and their free ranks
+    int32_t cslot[C::HS];              // their slots (the sorted keys during the incidence loop)
     int32_t frk[C::HS];                // slot -> free rank of the row (-1: Dirichlet)
     uint32_t msk[C::HS][NV];           // slot -> pass-i mask over incidences
     // items and folds first; once every fold is done the same bytes hold the
@@ -693,7 +700,6 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
             if (p.want_a) {
                 for (int h = g; h < C::HS; h += L) {
                     sm.row[h] = -1;
-                    sm.crow[h] = -1;
 #pragma unroll
                     for (int i = 0; i < NV; ++i) sm.msk[h][i] = 0u;
                 }
@@ -789,10 +795,19 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 // exact-zero items are skipped: x + (+-0) == x for x != 0, a zero
                 // prefix only changes the sign of a zero the next nonzero item
                 // absorbs, and an all-zero entry is dropped anyway (sparse.hpp:105)
+                // lanes walk their own nonzero items (a static loop over i ran each
+                // pass with a third of the lanes on Kuhn meshes: most items are 0)
+                uint32_t todo = 0;
 #pragma unroll
-                for (int i = 0; i < NV; ++i) {  // static i: R[i], FR[i] stay in their registers
-                    if (i == j_ || s[i] == 0.0) continue;
-                    const int32_t r = R[i], fr = FR[i];
+                for (int i = 0; i < NV; ++i) {
+                    sm.lr[g * NV + i] = R[i];
+                    sm.lfr[g * NV + i] = FR[i];
+                    todo |= (i != j_ && s[i] != 0.0) ? (1u << i) : 0u;
+                }
+#pragma unroll 1
+                for (; todo; todo &= todo - 1) {
+                    const int i = __ffs(todo) - 1;
+                    const int32_t r = sm.lr[g * NV + i], fr = sm.lfr[g * NV + i];
                     uint32_t h = ((uint32_t)r * 2654435761u) >> (32 - lg2c(C::HS));
                     int slot = -1;
 #pragma unroll 1
@@ -835,6 +850,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
             uint64_t meta = 0;  // staging: first entry (40 bits) | count of A | count of A(free, free)
             if (p.want_a) {
                 // ---- 4. the diagonal slot, the folds, rows ranked, zero drop
+                for (int h = g; h < C::HS; h += L) sm.crow[h] = -1;  // (held the lanes' rows until here)
                 if (g == 0 && act && m > 0) {
                     uint32_t h = ((uint32_t)c * 2654435761u) >> (32 - lg2c(C::HS));
 #pragma unroll 1
@@ -1361,18 +1377,15 @@ static int launch4(fl_ctx* ctx, ColParams& p) {
     return FL_OK;
 }
 
-// resident CTAs per SM the kernel is compiled for (registers); FL_V4_MINB=8|10
-// selects the 3-D variant (tuning experiments)
+// Resident CTAs per SM the kernel is compiled for (its register cap).  2-D: 8 CTAs
+// of 4 warps at 64 registers (C3 column pass 6.42 / 5.74 / 5.08 / 5.43 ms at
+// 5 / 6 / 8 / 10 CTAs: occupancy pays until the spills take over).  3-D: 10 CTAs
+// of 2 warps at 96 registers, the shared-memory limit (128 registers, 8 CTAs,
+// measured the same).
 template <int D, int L, int K>
 static int launch4_sel(fl_ctx* ctx, ColParams& p) {
-    if constexpr (D == 3) {
-        const char* e = std::getenv("FL_V4_MINB");
-        if (e && e[0] == '8')
-            return p.need_lift ? launch4<D, L, K, true, 8>(ctx, p) : launch4<D, L, K, false, 8>(ctx, p);
-        return p.need_lift ? launch4<D, L, K, true, 10>(ctx, p) : launch4<D, L, K, false, 10>(ctx, p);
-    } else {
-        return p.need_lift ? launch4<D, L, K, true, 4>(ctx, p) : launch4<D, L, K, false, 4>(ctx, p);
-    }
+    constexpr int MINB = D == 3 ? 10 : 8;
+    return p.need_lift ? launch4<D, L, K, true, MINB>(ctx, p) : launch4<D, L, K, false, MINB>(ctx, p);
 }
 
 // The column pass of fl_assemble on the label plan (the whole mesh or a column range).  p carries the outputs, the
