@@ -380,7 +380,7 @@ FL_API int fl_mesh_destroy(fl_mesh* mesh) {
     mesh->bcnt.release();
     mesh->stats.release();
     auto& lp = mesh->lp;
-    for (fl::DevBuf* b : {&lp.lab, &lp.ilab, &lp.lptr, &lp.linc, &lp.lel, &lp.lcnt, &lp.misc, &lp.cells, &lp.stage})
+    for (fl::DevBuf* b : {&lp.lab, &lp.lptr, &lp.linc, &lp.lel, &lp.misc, &lp.cells, &lp.stage})
         b->release();
     delete mesh;
     return FL_OK;

@@ -4,24 +4,29 @@
 // C3) number their nodes randomly.  Indexing the plan, the coordinates and the
 // partition by node id turns every access of the column pass into a random
 // DRAM sector: the id-space v3 pass read 109 GB on C5 for 3.6 GB of compulsory
-// traffic.  Here every node gets a LABEL, the order in which the element
-// stream first touches it (computed inside the count pass, no sort), and all
-// intermediate work runs in label order:
+// traffic.  Here every node gets a LABEL -- its place in the Morton order of the
+// nodes' coordinates (cells of ~8 nodes) -- and all intermediate work runs in
+// label order:
 //
-//   plan     k4_count     per-node incidence counts + first-touch labels
-//            k4_untouched labels for nodes no element references
-//            scan         label segments lptr = exclusive scan of counts by label
-//            k4_fill      (j << 30 | t) keys into the label segments; the
-//                         elements rewritten with vertex labels (lel)
+//   plan     k4_bbox / k4_cell / scan / k4_cell_scatter   labels (lab: node -> label)
+//            k4_fill      one pass over the elements: (j << 30 | t) keys into
+//                         fixed-capacity label segments (the per-label count is
+//                         the cursor: no count pass, no scan) and the elements
+//                         rewritten with vertex labels (lel); large 2-D meshes
+//                         go through buckets of labels (k4_bucket_scatter + k4_fill_b)
+//            k4_stats     nnz bound and maximum valence
 //   per call k4_xl        xl[label] = node coordinates + {node id, free rank}
 //            k_columns4   one group of L lanes per column (label), K incidences
 //                         per lane: element geometry computed in the kernel from
 //                         xl (no element-record round trip through HBM), the
 //                         reference's exact per-entry fold order, zero drop,
-//                         load vector, Dirichlet lift, A(free,free); entries
-//                         staged per tile of labels
-//            scans + k4_place  CSC column pointers in node-id order, staged
-//                         runs copied to their node-id positions, vectors
+//                         load vector, Neumann shares, Dirichlet lift,
+//                         A(free,free); entries staged per tile of labels
+//            k4_place     CSC column pointers in node-id order (scan + look-back),
+//                         staged runs copied to their node-id positions, vectors
+//
+// A column range (multi-GPU shard) labels its own nodes first, so the plan and the
+// column pass cover labels [0, n_owned) only.
 //
 // Labels never reach the output: rows are node ids, every fold runs in the
 // reference's (i*(d+1)+j, t) order with the original element index t, so the
@@ -47,109 +52,19 @@ __host__ __device__ constexpr int lg2c(int x) { return x <= 1 ? 0 : 1 + lg2c(x >
 // ===========================================================================
 // plan
 // ===========================================================================
-constexpr int kP4Block = 256, kP4Iters = 16;
+constexpr int kP4Block = 256;
 
-// misc buffer layout: u64 stats[4] (nnz bound, max valence, -, -), u32 label
-// counter, u32 error word
+// misc buffer layout: u64 stats[4] (nnz bound, max valence, -, -), u32 spare,
+// u32 error word (read back as the high half of the fifth u64)
 struct P4Misc {
     unsigned long long stats[4];
-    uint32_t lctr;
+    uint32_t spare;
     uint32_t err;
 };
 
-// Counts per node and first-touch labels.  Block b covers entries
-// [b*256*16, (b+1)*256*16) (blocks issued in element order).  Lanes holding
-// the same node are grouped with match_any; the group leader adds the group's
-// count, and the one whose add returns 0 is the node's first toucher.  Labels
-// are handed out per block (one atomic), warp-major then iteration then lane.
-__global__ void __launch_bounds__(kP4Block)
-k4_count(int64_t n_entries, int32_t n_nodes, const int32_t* __restrict__ elems,
-         int32_t* __restrict__ cnt, int32_t* __restrict__ lab, int32_t* __restrict__ ilab,
-         P4Misc* __restrict__ misc) {
-    __shared__ int32_t wsum[kP4Block / 32];
-    __shared__ int32_t s_base;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned lower = (1u << lane) - 1;
-    const int64_t b0 = (int64_t)blockIdx.x * kP4Block * kP4Iters;
-    int32_t fv[kP4Iters];
-    unsigned bal[kP4Iters];
-    int wtot = 0;
-    uint32_t err = 0;
-#pragma unroll
-    for (int k = 0; k < kP4Iters; ++k) {
-        const int64_t e = b0 + (int64_t)k * kP4Block + threadIdx.x;
-        int32_t key = -1;
-        if (e < n_entries) {
-            const int32_t v = __ldg(elems + e);
-            if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
-            else key = v;
-        }
-        const unsigned g = __match_any_sync(kFull, key);
-        bool first = false;
-        if (key >= 0 && (g & lower) == 0) first = atomicAdd(cnt + key, __popc(g)) == 0;
-        fv[k] = key;
-        bal[k] = __ballot_sync(kFull, first);
-        wtot += __popc(bal[k]);
-    }
-    if (__any_sync(kFull, err != 0) && lane == 0) atomicOr(&misc->err, DERR_INDEX);
-    if (lane == 0) wsum[w] = wtot;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int32_t s = 0;
-#pragma unroll
-        for (int i = 0; i < kP4Block / 32; ++i) {
-            const int32_t x = wsum[i];
-            wsum[i] = s;
-            s += x;
-        }
-        s_base = s ? (int32_t)atomicAdd(&misc->lctr, (uint32_t)s) : 0;
-    }
-    __syncthreads();
-    int32_t base = s_base + wsum[w];
-#pragma unroll
-    for (int k = 0; k < kP4Iters; ++k) {
-        if ((bal[k] >> lane) & 1u) {
-            const int32_t lb = base + __popc(bal[k] & lower);
-            lab[fv[k]] = lb;
-            ilab[lb] = fv[k];
-        }
-        base += __popc(bal[k]);
-    }
-}
-
-// nodes no element references (their columns are empty) take the last labels
-__global__ void __launch_bounds__(kP4Block)
-k4_untouched(int32_t n_nodes, const int32_t* __restrict__ cnt, int32_t* __restrict__ lab,
-             int32_t* __restrict__ ilab, P4Misc* __restrict__ misc) {
-    __shared__ int32_t wsum[kP4Block / 32];
-    __shared__ int32_t s_base;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned lower = (1u << lane) - 1;
-    const int32_t v = blockIdx.x * kP4Block + threadIdx.x;
-    const bool un = v < n_nodes && __ldg(cnt + v) == 0;
-    const unsigned b = __ballot_sync(kFull, un);
-    if (lane == 0) wsum[w] = __popc(b);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int32_t s = 0;
-        for (int i = 0; i < kP4Block / 32; ++i) {
-            const int32_t x = wsum[i];
-            wsum[i] = s;
-            s += x;
-        }
-        s_base = s ? (int32_t)atomicAdd(&misc->lctr, (uint32_t)s) : 0;
-    }
-    __syncthreads();
-    if (un) {
-        const int32_t lb = s_base + wsum[w] + __popc(b & lower);
-        lab[v] = lb;
-        ilab[lb] = v;
-    }
-}
-
-// ---- spatial labels (default): nodes bucketed by the Morton cell of their
-// coordinates (cells of ~64 nodes along a Z-curve over the bounding box), in any
-// element order -- C3 permutes its elements, so first-touch order is random there.
+// ---- labels: nodes bucketed by the Morton cell of their coordinates (cells of ~8
+// nodes along a Z-curve over the bounding box), whatever the element order (C3
+// permutes its elements: a first-touch order of the element stream is random there).
 __global__ void k4_bbox(int32_t n, int dim, const double* __restrict__ nodes, double* __restrict__ part) {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
@@ -232,12 +147,9 @@ __global__ void k4_cell(int32_t n, int dim, int bits, int nparts, const double* 
 
 // label = the node's place in its cell's run (cursor seeded with the cell offsets)
 __global__ void k4_cell_scatter(int32_t n, const int32_t* __restrict__ cell, int32_t* __restrict__ cursor,
-                                int32_t* __restrict__ lab, int32_t* __restrict__ ilab) {
-    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const int32_t lb = atomicAdd(cursor + __ldg(cell + v), 1);
-        lab[v] = lb;
-        ilab[lb] = v;
-    }
+                                int32_t* __restrict__ lab) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        lab[v] = atomicAdd(cursor + __ldg(cell + v), 1);
 }
 
 // (j << 30 | t) keys into the label segments and the elements with vertex labels
@@ -1283,31 +1195,12 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     const bool sharded = c0 != 0 || c1 != N;
     const int64_t n_entries = (int64_t)mesh->n_elems * nv;
     FL_TRY(lp.lab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-    FL_TRY(lp.ilab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.lptr.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.lel.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(n_entries, 4)));
     FL_TRY(lp.misc.ensure(sizeof(P4Misc)));
     P4Misc* misc = lp.misc.as<P4Misc>();
     int32_t* lab = lp.lab.as<int32_t>();
-    int32_t* ilab = lp.ilab.as<int32_t>();
-    const char* lenv = std::getenv("FL_LABELS");
-    if (lenv && lenv[0] == 'f' && !sharded) {
-        // first touch in element order (no coordinates involved; its per-node
-        // counts only detect the first toucher)
-        FL_TRY(lp.lcnt.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-        int32_t* cnt = lp.lcnt.as<int32_t>();
-        FL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)N + 1), s));
-        FL_CUDA(cudaMemsetAsync(misc, 0, sizeof(P4Misc), s));
-        const int64_t cblocks = (n_entries + kP4Block * kP4Iters - 1) / (kP4Block * kP4Iters);
-        if (n_entries > 0) {
-            k4_count<<<(int)cblocks, kP4Block, 0, s>>>(n_entries, N, mesh->elems.as<int32_t>(), cnt, lab, ilab, misc);
-            count_launch(ctx);
-        }
-        if (N > 0) {
-            k4_untouched<<<div_up(N, kP4Block), kP4Block, 0, s>>>(N, cnt, lab, ilab, misc);
-            count_launch(ctx);
-        }
-    } else if (N > 0) {
+    if (N > 0) {
         // Morton cells of ~cn nodes (FL_CELL_NODES, default 8: C5 column pass 18.2 / 17.8
         // / 17.7 ms at 64 / 8 / 1, plan +0.6 ms at 1): 2^(dim*bits) cells
         const int dim = mesh->dim;
@@ -1333,7 +1226,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
         FL_CUDA(launch_scan<int32_t>(ncell, [cc] __device__(int64_t i) { return (int64_t)cc[i]; }, coff,
                                      ctx->scan_ws.p, s));
         count_launch(ctx);
-        k4_cell_scatter<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, cellv, coff, lab, ilab);
+        k4_cell_scatter<<<std::min(div_up(N, 256), ctx->sm_count * 8), 256, 0, s>>>(N, cellv, coff, lab);
         count_launch(ctx);
     }
     // Segment capacity: a re-plan keeps the last known valence class (a topology
