@@ -195,6 +195,7 @@ FL_API int fl_create(int device, fl_ctx** out) {
     const char* ov = std::getenv("FL_OVERLAP");
     ctx->overlap = !(ov && ov[0] == '0');
     FL_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+    FL_TRY(v4_init_consts(ctx));
     const char* prof = std::getenv("FL_PROFILE");
     ctx->profile = prof && prof[0] == '1';
     if (ctx->profile)

@@ -529,8 +529,8 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
     static_assert(sizeof(Padded<V4Smem<D, L, K, LIFT>>) % 128 == 32 ||
                       sizeof(Padded<V4Smem<D, L, K, LIFT>>) % 128 == 48,
                   "group stride must be 8 (+-) banks off a multiple of 32");
-    const Recip R3 = recip(3.0);
-    const Recip R6 = recip(6.0);
+    const Recip R3 = p.r3;
+    const Recip R6 = p.r6;
 
     while (true) {
         int64_t tile = 0;
@@ -1129,6 +1129,24 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
 // ===========================================================================
 int v4_lanes(int dim) { return dim == 2 ? 16 : 32; }  // incidences per column the kernel takes
 
+// the divisor halves of x / 3 and x / 6 (fl::recip: device instructions), once per context
+__global__ void k4_recip_consts(double* out) {
+    const Recip a = recip(3.0), b = recip(6.0);
+    out[0] = a.b;
+    out[1] = a.r;
+    out[2] = b.b;
+    out[3] = b.r;
+}
+int v4_init_consts(fl_ctx* ctx) {
+    double* d = nullptr;
+    FL_CUDA(cudaMalloc(&d, sizeof(double) * 4));
+    k4_recip_consts<<<1, 1, 0, ctx->stream>>>(d);
+    FL_CUDA(cudaMemcpyAsync(ctx->recip_consts, d, sizeof(double) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    FL_CUDA(cudaStreamSynchronize(ctx->stream));
+    FL_CUDA(cudaFree(d));
+    return FL_OK;
+}
+
 // slots per label segment for a mesh of maximum valence max_inc: the column
 // kernel variant's incidences per column (2-D: 8 lanes x 1 or 2; 3-D: 8 x 4)
 int v4_cap(int dim, int max_inc) { return dim == 2 ? (max_inc <= 8 ? 8 : 16) : 32; }
@@ -1297,6 +1315,8 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     p.vst = res->v4[1].as<double4>();
     p.lel = lp.lel.as<int32_t>();
     p.inc_ptr = nullptr;
+    p.r3 = Recip{ctx->recip_consts[0], ctx->recip_consts[1]};
+    p.r6 = Recip{ctx->recip_consts[2], ctx->recip_consts[3]};
     p.lab = lp.lab.as<int32_t>();
     p.lcnt = lp.lptr.as<int32_t>();
     p.lcap = lp.cap;

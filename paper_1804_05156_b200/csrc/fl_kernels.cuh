@@ -85,6 +85,8 @@ struct ColParams {
     // node's coordinates and {node id, free rank or -1} in .w; vst[label] =
     // {b, u0, b - A u0, 0}
     const int32_t* lel;
+    Recip r3, r6;         // recip(3.0), recip(6.0) computed once per context (kernel parameters
+                          // are constant-bank operands: no registers held across the column loop)
     const int32_t* lab;   // node id -> label
     const int32_t* lcnt;  // incidences per label; label l's keys at inc[l * lcap ..]
     int32_t lcap;
@@ -136,6 +138,7 @@ int matvec_device(fl_ctx* ctx, int32_t m, int32_t n, const int32_t* col_ptr, con
 size_t column_smem_bytes();
 // v4 (fl_columns4.cu)
 int v4_lanes(int dim);
+int v4_init_consts(fl_ctx* ctx);
 int v4_cap(int dim, int max_inc);
 int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync);
 int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res);
