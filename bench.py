@@ -349,11 +349,12 @@ def run_ours(args, rank: int, world: int):
     b_sys = configs.system_bytes(d, N, NT, nnz, n_free, nnz_ff)
     f_bytes = 8 * NT * (d + 1) if ff.kind == _lib.FIELD_SAMPLES else 0
     # the column kernel's own compulsory bytes (this rank): label-plan keys and
-    # relabelled elements read once, label-ordered nodes read once, staged entries
-    # and per-label vectors written once
-    frac_el = 1.0 if world == 1 else min(1.0, ncol_l / max(N, 1) * 1.0)
-    kern_bytes = (int(frac_el * (8 * (d + 1) * NT + f_bytes)) + 32 * ncol_l
-                  + 12 * nnz_l + 12 * nnz_ff_l + 32 * ncol_l + 8 * ncol_l)
+    # relabelled elements read once (the share of the elements touching the
+    # rank's columns), label-ordered node records of every node and the per-label
+    # counts read once, 16-byte staged entries and per-node vector records written once
+    frac_el = 1.0 if world == 1 else min(1.0, 1.0 - (1.0 - ncol_l / max(N, 1)) ** (d + 1))
+    kern_bytes = (int(frac_el * 4 * (d + 1) * NT) + 4 * (d + 1) * int(NT * ncol_l / max(N, 1)) + f_bytes
+                  + 32 * N + 4 * ncol_l + 16 * nnz_l + 32 * ncol_l)
     peak, peak_kind = peaks()
     # achieved = B_SL / t, t = the measured assembly (the whole step)
     achieved = b_sl / (ms * 1e-3) / 1e9

@@ -10,6 +10,9 @@ for c in sys.argv[1:]:
     d = collections.defaultdict(dict)
     for r in rows[1:]:
         d[(int(r[ii]), r[ki][:40])][r[mi]] = float(r[vi].replace(",", ""))
+    starts = [i for (i, k) in sorted(d) if k.startswith("k4_bbox")]
+    if starts:  # the last (steady-state) step only
+        d = {ik: m for ik, m in d.items() if ik[0] >= starts[-1]}
     tot = sum(m.get("gpu__time_duration.sum", 0) for m in d.values()) / 1e6
     print(c, f"total {tot:.3f} ms over {len(d)} launches")
     for (i, k), m in sorted(d.items()):
