@@ -171,19 +171,22 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t err = 0;
     for (int64_t e0 = warp * 32 * U; e0 < n_entries; e0 += nwarps * 32 * U) {
-        int32_t key[U];
+        int32_t key[U], vtx[U];
+        bool tch[U];
         unsigned grp[U];
         int32_t pos[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t e = e0 + u * 32 + lane;
             key[u] = -1;
+            vtx[u] = -1;
+            tch[u] = false;
             if (e < n_entries) {
                 const int32_t v = __ldg(elems + e);
                 // a shard skips the elements that touch none of its columns: no
                 // label gather, no lel row (the column pass never reads it)
                 bool touched = true;
-                if (sharded) {
+                if (sharded && nv != 4) {  // (nv == 4: the element's four lanes vote below)
                     const int64_t t0 = (int64_t)entry_elem(e, nv) * nv;
                     touched = false;
                     for (int i = 0; i < nv; ++i) {
@@ -191,6 +194,26 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
                         touched = touched || (w >= c0 && w < c1);
                     }
                 }
+                vtx[u] = v;
+                tch[u] = touched;
+            }
+        }
+        if (sharded && nv == 4) {
+            // a tetrahedron's entries sit in four consecutive lanes (rounds start at
+            // multiples of 32): touched = any of them owned
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool own = vtx[u] >= c0 && vtx[u] < c1;
+                const unsigned b = __ballot_sync(kFull, own);
+                tch[u] = ((b >> (lane & ~3)) & 0xFu) != 0u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = e0 + u * 32 + lane;
+            if (e < n_entries) {
+                const int32_t v = vtx[u];
+                const bool touched = tch[u];
                 if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
                 if (touched) {
                     int32_t lb = -1;
