@@ -152,6 +152,15 @@ __global__ void k4_cell_scatter(int32_t n, const int32_t* __restrict__ cell, int
         lab[v] = atomicAdd(cursor + __ldg(cell + v), 1);
 }
 
+// lel rows are 4 labels wide in both dimensions (a triangle's row is one aligned
+// 16-byte load in the column kernel, not three 4-byte ones: the 2-D kernel is bound
+// by L1 wavefronts)
+__device__ __forceinline__ int64_t lel_index(int64_t e, int nv) {
+    if (nv == 4) return e;
+    const int32_t t = entry_elem(e, nv);
+    return (int64_t)t * 4 + (e - (int64_t)t * nv);
+}
+
 // (j << 30 | t) keys into the label segments and the elements with vertex labels
 // (lel), one pass: label l owns the `cap` slots linc[l * cap ..], its count
 // cnt[l] (zeroed before) is the fill cursor -- no separate count pass, no scan.
@@ -218,7 +227,7 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
                 if (touched) {
                     int32_t lb = -1;
                     if ((uint32_t)v < (uint32_t)n_nodes) lb = __ldg(lab + v);
-                    lel[e] = lb;
+                    lel[lel_index(e, nv)] = lb;
                     if (v >= c0 && v < c1) key[u] = lb;  // keys for this shard's columns only
                 }
             }
@@ -288,7 +297,7 @@ k4_bucket_scatter(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, int32_
             if ((uint32_t)v >= (uint32_t)n_nodes) err = DERR_INDEX;
             if (touched) {
                 if ((uint32_t)v < (uint32_t)n_nodes) lv[k] = __ldg(lab + v);
-                lel[e] = lv[k];
+                lel[lel_index(e, nv)] = lv[k];
             }
             if (v < c0 || v >= c1) lv[k] = -1;  // staged for this shard's columns only
             if (lv[k] >= 0) {
@@ -654,13 +663,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                 int4 v = make_int4(0, 0, 0, 0);
                 if (kk * L + g < m) {
                     const int32_t tt = (int32_t)(key_at(kk) & 0x3FFFFFFFu);
-                    if constexpr (D == 3) {
-                        v = __ldg(reinterpret_cast<const int4*>(p.lel) + tt);
-                    } else {
-                        v.x = __ldg(p.lel + (size_t)tt * NV);
-                        v.y = __ldg(p.lel + (size_t)tt * NV + 1);
-                        v.z = __ldg(p.lel + (size_t)tt * NV + 2);
-                    }
+                    v = __ldg(reinterpret_cast<const int4*>(p.lel) + tt);  // (2-D: .w unused)
                 }
                 return v;
             };
@@ -1237,7 +1240,7 @@ int v4_plan(fl_ctx* ctx, fl_mesh* mesh, bool sync) {
     const int64_t n_entries = (int64_t)mesh->n_elems * nv;
     FL_TRY(lp.lab.ensure(sizeof(int32_t) * ((size_t)N + 1)));
     FL_TRY(lp.lptr.ensure(sizeof(int32_t) * ((size_t)N + 1)));
-    FL_TRY(lp.lel.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(n_entries, 4)));
+    FL_TRY(lp.lel.ensure(sizeof(int32_t) * 4 * (size_t)std::max<int32_t>(mesh->n_elems, 1)));
     FL_TRY(lp.misc.ensure(sizeof(P4Misc)));
     P4Misc* misc = lp.misc.as<P4Misc>();
     int32_t* lab = lp.lab.as<int32_t>();
