@@ -220,6 +220,57 @@ def test_async_replan_after_new_connectivity(ctx):
     assert _bits(got.values) == _bits(want.values)
 
 
+def test_replan_valence_class_change(ctx):
+    """The label plan's segments hold 8 keys per node while the mesh's valence is
+    <= 8 (2-D).  New connectivity with a valence-12 node, re-planned asynchronously:
+    the first assembly overflows the segments and is redone on the general kernel,
+    the next one plans 16-key segments and stays on the fast kernel -- all bitwise."""
+    from tests.meshes import fix_orientation
+    k = 12
+    ang = 2 * np.pi * np.arange(k) / k
+    nodes = np.vstack([[0.0, 0.0], np.stack([np.cos(ang), np.sin(ang)], 1)])
+    ring = np.array([[1 + i, 1 + (i + 1) % k, 1 + (i + 2) % k] for i in range(k)], dtype=np.int32)
+    fan = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)], dtype=np.int32)
+    low = Mesh(2, nodes, fix_orientation(2, nodes, ring))    # valence 3
+    high = Mesh(2, nodes, fix_orientation(2, nodes, fan))    # node 0: valence 12
+    want = fl.assemble_blockwise(high, ctx=ctx)
+    dm = low.device(ctx)
+    dm.plan()
+    fl.run(low, _lib.OUT_STIFFNESS, ctx=ctx, device_mesh=dm).sizes()
+    fe = np.ascontiguousarray(high.elems, dtype=np.int32)
+    _lib.check(_lib.lib().fl_mesh_set_elems(ctx.handle, dm.handle, fe.ctypes.data, _lib.MEM_HOST))
+    for _ in range(3):
+        got = fl.run(high, _lib.OUT_STIFFNESS | _lib.REPLAN, ctx=ctx, device_mesh=dm).matrix()
+        np.testing.assert_array_equal(got.col_ptr, want.col_ptr)
+        np.testing.assert_array_equal(got.row_idx, want.row_idx)
+        assert _bits(got.values) == _bits(want.values)
+
+
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_replan_side_stream(overlap, monkeypatch, ref_which):
+    """FL_OVERLAP: on a re-plan the partition + FaceLists run on the context's side
+    stream beside the label plan (1, default) or on the one stream (0) -- same bits."""
+    from paper_1804_05156_b200 import configs
+    monkeypatch.setenv("FL_OVERLAP", overlap)
+    c2 = fl.Context(0)
+    cfg = configs.build("C5", n=10, f_mode="samples")
+    m = cfg.mesh
+    coef = configs.host_samples(m, rule=1, kind=7)
+    a = po.assemble_blockwise(m.dim, m.nodes, m.elems, coef=coef, which=ref_which)
+    d, f, _, _ = po.partition_boundary(m.dim, m.nodes, m.elems, m.bd_flags, which=ref_which)
+    res = fl.AssemblyResult(c2)
+    dm = m.device(c2)
+    for what in (_lib.OUT_SYSTEM, _lib.OUT_SYSTEM | _lib.REPLAN, _lib.OUT_SYSTEM | _lib.REPLAN):
+        r = fl.run(m, what, f=cfg.f, coef=coef, g_dirichlet="x", ctx=c2, result=res, device_mesh=dm)
+        got = r.matrix()
+        np.testing.assert_array_equal(got.col_ptr, a.col_ptr)
+        assert _bits(got.values) == _bits(a.values)
+        np.testing.assert_array_equal(r.partition().free_nodes, f)
+        np.testing.assert_array_equal(r.partition().dirichlet_nodes, d)
+        aff = po.submatrix(a, f, f, which=ref_which)
+        assert _bits(r.matrix_ff().values) == _bits(aff.values)
+
+
 @pytest.mark.parametrize("world", [1, 3])
 def test_result_counts_async_matches_sizes(world, ctx):
     """fl_result_counts_async (the payload of the NCCL nnz-offset exchange)."""
