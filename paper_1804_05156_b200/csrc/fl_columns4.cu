@@ -449,8 +449,18 @@ struct alignas(16) Padded {
 // one staged entry: 16 bytes {row, free rank of the row or -1, value} (one run per
 // column: the placement gathers 64-byte granules at random, so row and value
 // share them)
-__device__ __forceinline__ void stage_entry(const ColParams& p, int64_t o, int32_t row, int32_t frk, double v) {
-    reinterpret_cast<double2*>(p.st_a_row)[o] = make_double2(__hiloint2double(frk, row), v);
+// Entry k of local column lc lives in the column's first-level run (kStageFirst
+// entries at lc * kStageFirst: 128 bytes, enough for most columns, read by the
+// placement as a dense stream) or, beyond that, in its overflow run.
+constexpr int kStageFirst = 8;
+__device__ __forceinline__ double2* stage_slot(const ColParams& p, int64_t lc, int k) {
+    double2* a = reinterpret_cast<double2*>(p.st_a_row);
+    double2* b = reinterpret_cast<double2*>(p.st_a_val);
+    return k < kStageFirst ? a + lc * kStageFirst + k : b + lc * (p.tile_cap - kStageFirst) + (k - kStageFirst);
+}
+__device__ __forceinline__ void stage_entry(const ColParams& p, int64_t lc, int k, int32_t row, int32_t frk,
+                                            double v) {
+    *stage_slot(p, lc, k) = make_double2(__hiloint2double(frk, row), v);
 }
 
 __device__ __forceinline__ double4 ld_xl(const double4* p) {
@@ -569,8 +579,6 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
         if (lane == 0) tile = atomicAdd(p.ticket, 1u);
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= p.n_tiles) break;
-        const int64_t sbase = tile * p.tile_cap;
-        int run_a = 0;  // warp-uniform: entries staged so far in this tile
         bool bad = false;
         const int32_t lc0 = (int32_t)(tile * C::WTC);
         const int ncol_t = (int)min((int64_t)C::WTC, (int64_t)p.n_cols - lc0);
@@ -785,7 +793,10 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
             // apply_neumann (system.hpp:123-172): b + the node's accumulated face shares
             if (p.nadd && act && p.is_neu[c]) b = b + p.nadd[c - p.c_begin];
             double ylift = 0.0;
-            uint64_t meta = 0;  // staging: first entry (40 bits) | count of A | count of A(free, free)
+            uint64_t meta = 0;  // count of A << 40 | count of A(free, free) << 48
+            // the column's staged run sits at its NODE ID (the placement then reads the
+            // staging as a stream; the scattered writes cost this kernel nothing)
+            const int64_t cbase = c - p.c_begin;
             if (p.want_a) {
                 // ---- 4. the diagonal slot, the folds, rows ranked, zero drop
                 for (int h = g; h < C::HS; h += L) sm.crow[h] = -1;  // (held the lanes' rows until here)
@@ -903,23 +914,14 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                         kept = keptf = 0;
                     }
                     const int na = __popc(kept), nf = __popc(keptf);
-                    int pa = na;  // inclusive prefix over the groups (column order)
-#pragma unroll
-                    for (int o = L; o < 32; o <<= 1) {
-                        const int ya = __shfl_up_sync(kFull, pa, o);
-                        if (lane >= o) pa += ya;
-                    }
-                    const int tot_a = __shfl_sync(kFull, pa, 31);
-                    const int wa = run_a + pa - na;  // this column's first slot
-                    meta = (uint64_t)(sbase + wa) | ((uint64_t)na << 40) | ((uint64_t)nf << 48);
+                    meta = ((uint64_t)na << 40) | ((uint64_t)nf << 48);
 #pragma unroll
                     for (int ii = 0; ii < NI; ++ii) {
                         const int rk = rkv[ii];
                         if (rk < 0 || !((kept >> rk) & 1u)) continue;
-                        const int64_t o = sbase + wa + __popc(kept & ((1u << rk) - 1));
-                        stage_entry(p, o, rowv[ii], p.want_sys ? frkv[ii] : -1, accv[ii]);
+                        stage_entry(p, cbase, __popc(kept & ((1u << rk) - 1)), rowv[ii], p.want_sys ? frkv[ii] : -1,
+                                    accv[ii]);
                     }
-                    run_a += tot_a;
                 } else {
                 __syncwarp();
 #pragma unroll
@@ -988,15 +990,8 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                     na += __popc(__ballot_sync(kFull, keep) & gmask);
                     nf += __popc(__ballot_sync(kFull, keepf) & gmask);
                 }
-                int pa = na;  // inclusive prefix over the groups (column order)
-#pragma unroll
-                for (int o = L; o < 32; o <<= 1) {
-                    const int ya = __shfl_up_sync(kFull, pa, o);
-                    if (lane >= o) pa += ya;
-                }
-                const int tot_a = __shfl_sync(kFull, pa, 31);
-                int wa = run_a + pa - na;  // this column's first slot
-                meta = (uint64_t)(sbase + wa) | ((uint64_t)na << 40) | ((uint64_t)nf << 48);
+                int wa = 0;  // entries of this column staged so far
+                meta = ((uint64_t)na << 40) | ((uint64_t)nf << 48);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     const int qq = ch * L + g;
@@ -1007,12 +1002,10 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
                     const bool keep = in && v != 0.0;
                     const unsigned ba = __ballot_sync(kFull, keep) & gmask;
                     if (keep) {
-                        const int64_t o = sbase + wa + __popc(ba & lower);
-                        stage_entry(p, o, r, fr, v);
+                        stage_entry(p, cbase, wa + __popc(ba & lower), r, fr, v);
                     }
                     wa += __popc(ba);
                 }
-                run_a += tot_a;
                 }  // LIFT
             }
             // ---- per-column record, by NODE ID (the placement then streams it):
@@ -1063,7 +1056,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
     const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
     const int32_t ca = in ? (int32_t)((meta >> 40) & 0xFF) : 0;
     const int32_t cf = fr >= 0 ? (int32_t)((meta >> 48) & 0xFF) : 0;
-    const int64_t src = (int64_t)(meta & 0xFFFFFFFFFFull);
+    const int64_t src = v;  // the column's staged run (stage_slot)
     if (in) {
         if (p.want_b) p.b[v] = vs.x;
         if (p.want_sys) {
@@ -1107,7 +1100,6 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
     const int32_t ex = pre - ca;
     const int32_t d0 = __shfl_sync(kFull, pa, 0);
     if ((int64_t)d0 + total_w > p.cap_a) return;  // flagged above
-    const double2* srf = reinterpret_cast<const double2*>(p.st_a_row);
     const int cfree_l = fr >= 0 ? 1 : 0;
     int carry_k = -1, carry = 0;
     for (int32_t q0 = 0; q0 < total_w; q0 += 32) {
@@ -1127,8 +1119,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
         int2 rf = make_int2(0, -1);
         double val = 0.0;
         if (qq < total_w) {
-            const int64_t s = sk + (qq - ek);
-            const double2 rec = __ldcs(srf + s);  // {row | free rank << 32, value}
+            const double2 rec = __ldcs(stage_slot(p, sk, qq - ek));  // {row | free rank << 32, value}
             rf = make_int2(__double2loint(rec.x), __double2hiint(rec.x));
             val = rec.y;
             p.row_idx[d0 + qq] = rf.x;
@@ -1354,12 +1345,13 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
         count_launch(ctx);
     }
     // one staged run per column of 16-byte entries {row, free rank, value}
-    // (A(free, free) rides along); tile t's runs start at t * tile_cap
+    // (A(free, free) rides along), maxs slots at the column's node id
     p.n_tiles = (p.n_cols + wtc - 1) / wtc;
-    p.tile_cap = (int64_t)wtc * maxs;
-    FL_TRY(res->stage[0].ensure(sizeof(double2) * (size_t)p.n_tiles * (size_t)p.tile_cap));
+    p.tile_cap = maxs;  // slots per column: kStageFirst in stage[0], the rest in stage[1]
+    FL_TRY(res->stage[0].ensure(sizeof(double2) * ((size_t)p.n_cols + 1) * kStageFirst));
+    FL_TRY(res->stage[1].ensure(sizeof(double2) * ((size_t)p.n_cols + 1) * (size_t)(maxs - kStageFirst)));
     p.st_a_row = res->stage[0].as<int32_t>();
-    p.st_a_val = nullptr;
+    p.st_a_val = res->stage[1].as<double>();
     FL_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(uint32_t), s));
     // Neumann data: per-node face shares first (k_neumann_add on the label plan)
     p.nadd = nullptr;
