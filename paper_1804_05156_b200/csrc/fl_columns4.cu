@@ -1027,14 +1027,16 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
 // ===========================================================================
 // placement: label-ordered staging -> node-id-ordered CSC and vectors, one pass
 // ===========================================================================
-// Tile = 256 consecutive node ids (one per thread), tiles taken in order from a
-// ticket.  Each node's record vst[v] (written by k_columns4 at the node id) holds
-// its vectors and, packed in .w, the staging index and count of its A and
-// A(free, free) entries.  The column pointers are an exclusive scan over node ids
-// (block scan + decoupled look-back on (nnz_A, nnz_Aff) packed in 64 bits); a
-// warp's 32 consecutive columns are one contiguous destination run, copied with
-// every store instruction writing 32 consecutive entries.
-constexpr int kPlaceThreads = 256;
+// Tile = kPlaceItems sub-tiles of 256 consecutive node ids (one per thread and
+// sub-tile), tiles taken in order from a ticket.  Each node's record vst[v]
+// (written by k_columns4 at the node id) holds its vectors and, packed in .w, the
+// counts of its A and A(free, free) entries; its staged run sits at the node id
+// too (stage_slot).  The column pointers are an exclusive scan over node ids
+// (block scans + ONE decoupled look-back per tile on (nnz_A, nnz_Aff) packed in
+// 64 bits: with 256-node tiles a third of the kernel's stalls were blocks waiting
+// for their predecessor); a warp's 32 consecutive columns are one contiguous
+// destination run, copied with every store instruction writing 32 consecutive entries.
+constexpr int kPlaceThreads = 256, kPlaceItems = 4;
 
 __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t* __restrict__ status,
                                                           unsigned int* __restrict__ ticket) {
@@ -1045,99 +1047,116 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
-    const int32_t v = (int32_t)(tile * kPlaceThreads) + threadIdx.x;  // column c_begin + v
-    const bool in = v < N;
     // free ranks relative to the shard: free nodes below c_begin come first
     const int32_t fb = p.want_sys ? free_base(p) : 0;
-    int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + p.c_begin + v) : -1;
-    if (fr >= 0) fr -= fb;
-    double4 vs = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (in) vs = ld_xl(p.vst + v);  // the record of node v, in node order
-    const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
-    const int32_t ca = in ? (int32_t)((meta >> 40) & 0xFF) : 0;
-    const int32_t cf = fr >= 0 ? (int32_t)((meta >> 48) & 0xFF) : 0;
-    const int64_t src = v;  // the column's staged run (stage_slot)
-    if (in) {
-        if (p.want_b) p.b[v] = vs.x;
-        if (p.want_sys) {
-            p.u0[v] = vs.y;
-            p.b_mod[v] = vs.z;
-            if (fr >= 0) p.b_f[fr] = vs.z;
+    int32_t frv[kPlaceItems], cav[kPlaceItems], cfv[kPlaceItems];
+#pragma unroll
+    for (int k = 0; k < kPlaceItems; ++k) {
+        const int32_t v = (int32_t)(tile * kPlaceThreads * kPlaceItems) + k * kPlaceThreads + threadIdx.x;
+        const bool in = v < N;  // column c_begin + v
+        int32_t fr = (in && p.want_sys) ? __ldg(p.fidx + p.c_begin + v) : -1;
+        if (fr >= 0) fr -= fb;
+        double4 vs = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (in) vs = ld_xl(p.vst + v);  // the record of node v, in node order
+        const uint64_t meta = (uint64_t)__double_as_longlong(vs.w);
+        frv[k] = fr;
+        cav[k] = in ? (int32_t)((meta >> 40) & 0xFF) : 0;
+        cfv[k] = fr >= 0 ? (int32_t)((meta >> 48) & 0xFF) : 0;
+        if (in) {
+            if (p.want_b) p.b[v] = vs.x;
+            if (p.want_sys) {
+                p.u0[v] = vs.y;
+                p.b_mod[v] = vs.z;
+                if (fr >= 0) p.b_f[fr] = vs.z;
+            }
         }
     }
     if (!p.want_a) return;
     // exclusive prefix over node ids of (A count, A(free, free) count)
-    int64_t total;
-    int64_t excl = block_exclusive_sum<kPlaceThreads>((int64_t)ca | ((int64_t)cf << 32), warp_sums, total);
+    int64_t exv[kPlaceItems], run = 0;
+#pragma unroll
+    for (int k = 0; k < kPlaceItems; ++k) {
+        int64_t total;
+        exv[k] = run + block_exclusive_sum<kPlaceThreads>((int64_t)cav[k] | ((int64_t)cfv[k] << 32), warp_sums, total);
+        run += total;
+    }
     if (threadIdx.x < 32) {
-        const uint64_t e = warp_lookback(status, tile, (uint64_t)total);
+        const uint64_t e = warp_lookback(status, tile, (uint64_t)run);
         if (threadIdx.x == 0) s_excl = (int64_t)e;
     }
     __syncthreads();
-    excl += s_excl;
-    const int32_t pa = (int32_t)(excl & 0xFFFFFFFF), pf = (int32_t)(excl >> 32);
-    if (in) {
-        p.col_ptr[v] = pa;
-        if (fr >= 0) p.ff_col_ptr[fr] = pf;
-        if (v == N - 1) {
-            p.col_ptr[N] = pa + ca;
-            if (p.want_sys)  // free_rank[c_begin + N] - free_rank[c_begin] free columns
-                p.ff_col_ptr[__ldg(p.fidx + (int64_t)p.n_nodes + 1 + p.c_begin + N) - fb] = pf + cf;
+    const int64_t tile_excl = s_excl;
+#pragma unroll 1
+    for (int k = 0; k < kPlaceItems; ++k) {
+        const int32_t v = (int32_t)(tile * kPlaceThreads * kPlaceItems) + k * kPlaceThreads + threadIdx.x;
+        const bool in = v < N;
+        const int32_t fr = frv[k], ca = cav[k], cf = cfv[k];
+        const int64_t excl = exv[k] + tile_excl;
+        const int32_t pa = (int32_t)(excl & 0xFFFFFFFF), pf = (int32_t)(excl >> 32);
+        if (in) {
+            p.col_ptr[v] = pa;
+            if (fr >= 0) p.ff_col_ptr[fr] = pf;
+            if (v == N - 1) {
+                p.col_ptr[N] = pa + ca;
+                if (p.want_sys)  // free_rank[c_begin + N] - free_rank[c_begin] free columns
+                    p.ff_col_ptr[__ldg(p.fidx + (int64_t)p.n_nodes + 1 + p.c_begin + N) - fb] = pf + cf;
+            }
+            if ((int64_t)pa + ca > p.cap_a || (p.want_sys && (int64_t)pf + cf > p.cap_ff))
+                atomicOr(p.err, DERR_CAPACITY);
         }
-        if ((int64_t)pa + ca > p.cap_a || (p.want_sys && (int64_t)pf + cf > p.cap_ff)) atomicOr(p.err, DERR_CAPACITY);
-    }
-    // the warp's 32 columns are one contiguous run of A: every store writes 32
-    // consecutive entries; A(free, free) takes the entries with a free row in a
-    // free column, at the column's pointer + their rank among them
-    int32_t pre = ca;  // inclusive prefix over the warp's lanes
+        // the warp's 32 columns are one contiguous run of A: every store writes 32
+        // consecutive entries; A(free, free) takes the entries with a free row in a
+        // free column, at the column's pointer + their rank among them
+        int32_t pre = ca;  // inclusive prefix over the warp's lanes
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(kFull, pre, o);
-        if (lane >= o) pre += y;
-    }
-    const int32_t total_w = __shfl_sync(kFull, pre, 31);
-    if (total_w == 0) return;
-    const int32_t ex = pre - ca;
-    const int32_t d0 = __shfl_sync(kFull, pa, 0);
-    if ((int64_t)d0 + total_w > p.cap_a) return;  // flagged above
-    const int cfree_l = fr >= 0 ? 1 : 0;
-    int carry_k = -1, carry = 0;
-    for (int32_t q0 = 0; q0 < total_w; q0 += 32) {
-        const int32_t qq = q0 + lane;
-        // largest k with ex[k] <= qq (lanes with len 0 share prefixes: the search
-        // lands on the last of them, whose run holds qq)
-        int k = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const int32_t total_w = __shfl_sync(kFull, pre, 31);
+        if (total_w == 0) continue;
+        const int32_t ex = pre - ca;
+        const int32_t d0 = __shfl_sync(kFull, pa, 0);
+        if ((int64_t)d0 + total_w > p.cap_a) continue;  // flagged above
+        const int cfree_l = fr >= 0 ? 1 : 0;
+        int carry_k = -1, carry = 0;
+        for (int32_t q0 = 0; q0 < total_w; q0 += 32) {
+            const int32_t qq = q0 + lane;
+            // largest kk with ex[kk] <= qq (lanes with len 0 share prefixes: the search
+            // lands on the last of them, whose run holds qq)
+            int kk = 0;
 #pragma unroll
-        for (int stp = 16; stp > 0; stp >>= 1) {
-            const int32_t ek = __shfl_sync(kFull, ex, k + stp);
-            if (ek <= qq) k += stp;
+            for (int stp = 16; stp > 0; stp >>= 1) {
+                const int32_t ek = __shfl_sync(kFull, ex, kk + stp);
+                if (ek <= qq) kk += stp;
+            }
+            const int32_t ek = __shfl_sync(kFull, ex, kk);
+            const int64_t sk = __shfl_sync(kFull, v, kk);  // the column whose staged run holds qq
+            const int32_t pfk = __shfl_sync(kFull, pf, kk);
+            const int cfree = __shfl_sync(kFull, cfree_l, kk);
+            int2 rf = make_int2(0, -1);
+            double val = 0.0;
+            if (qq < total_w) {
+                const double2 rec = __ldcs(stage_slot(p, sk, qq - ek));  // {row | free rank << 32, value}
+                rf = make_int2(__double2loint(rec.x), __double2hiint(rec.x));
+                val = rec.y;
+                p.row_idx[d0 + qq] = rf.x;
+                p.values[d0 + qq] = val;
+            }
+            const bool isf = qq < total_w && p.want_sys && cfree && rf.y >= 0;
+            const unsigned bal = __ballot_sync(kFull, isf);
+            const int start = ek > q0 ? (int)(ek - q0) : 0;  // column kk's first lane in this round
+            const unsigned below = (1u << lane) - 1, before = (1u << start) - 1;
+            const int rank = __popc(bal & below & ~before) + (kk == carry_k ? carry : 0);
+            if (isf) {
+                p.ff_row_idx[pfk + rank] = rf.y;
+                p.ff_values[pfk + rank] = val;
+            }
+            // the column holding lane 31 may continue into the next round
+            const int k31 = __shfl_sync(kFull, kk, 31), st31 = __shfl_sync(kFull, start, 31);
+            carry = (k31 == carry_k ? carry : 0) + __popc(bal & ~((1u << st31) - 1));
+            carry_k = k31;
         }
-        const int32_t ek = __shfl_sync(kFull, ex, k);
-        const int64_t sk = __shfl_sync(kFull, src, k);
-        const int32_t pfk = __shfl_sync(kFull, pf, k);
-        const int cfree = __shfl_sync(kFull, cfree_l, k);
-        int2 rf = make_int2(0, -1);
-        double val = 0.0;
-        if (qq < total_w) {
-            const double2 rec = __ldcs(stage_slot(p, sk, qq - ek));  // {row | free rank << 32, value}
-            rf = make_int2(__double2loint(rec.x), __double2hiint(rec.x));
-            val = rec.y;
-            p.row_idx[d0 + qq] = rf.x;
-            p.values[d0 + qq] = val;
-        }
-        const bool isf = qq < total_w && p.want_sys && cfree && rf.y >= 0;
-        const unsigned bal = __ballot_sync(kFull, isf);
-        const int start = ek > q0 ? (int)(ek - q0) : 0;  // column k's first lane in this round
-        const unsigned below = (1u << lane) - 1, before = (1u << start) - 1;
-        const int rank = __popc(bal & below & ~before) + (k == carry_k ? carry : 0);
-        if (isf) {
-            p.ff_row_idx[pfk + rank] = rf.y;
-            p.ff_values[pfk + rank] = val;
-        }
-        // the column holding lane 31 may continue into the next round
-        const int k31 = __shfl_sync(kFull, k, 31), st31 = __shfl_sync(kFull, start, 31);
-        carry = (k31 == carry_k ? carry : 0) + __popc(bal & ~((1u << st31) - 1));
-        carry_k = k31;
     }
 }
 
@@ -1375,7 +1394,7 @@ int v4_columns(fl_ctx* ctx, fl_mesh* mesh, ColParams& p, fl_result* res) {
     if (ctx->profile) FL_CUDA(cudaEventRecord(ctx->ev[7], s));
     // placement: column pointers in node-id order, the copy and the vectors, one pass
     if (p.n_cols > 0) {
-        const int64_t ptiles = ((int64_t)p.n_cols + kPlaceThreads - 1) / kPlaceThreads;
+        const int64_t ptiles = ((int64_t)p.n_cols + kPlaceThreads * kPlaceItems - 1) / (kPlaceThreads * kPlaceItems);
         FL_TRY(res->v4[2].ensure(sizeof(uint64_t) * (size_t)(ptiles + 2)));
         uint64_t* status = res->v4[2].as<uint64_t>();
         FL_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)(ptiles + 2), s));
