@@ -21,9 +21,9 @@
 //                         xl (no element-record round trip through HBM), the
 //                         reference's exact per-entry fold order, zero drop,
 //                         load vector, Neumann shares, Dirichlet lift,
-//                         A(free,free); entries staged per tile of labels
+//                         A(free,free); entries staged at the column's node id
 //            k4_place     CSC column pointers in node-id order (scan + look-back),
-//                         staged runs copied to their node-id positions, vectors
+//                         staged runs streamed to their CSC positions, vectors
 //
 // A column range (multi-GPU shard) labels its own nodes first, so the plan and the
 // column pass cover labels [0, n_owned) only.
