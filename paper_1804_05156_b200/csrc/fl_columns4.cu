@@ -179,11 +179,26 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t err = 0;
+    // persistent warps: the next iteration's vertex ids are loaded one iteration
+    // ahead (the chain per iteration is then label gather -> atomic -> store)
+    int32_t vnext[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t e = warp * 32 * U + u * 32 + lane;
+        vnext[u] = e < n_entries ? __ldg(elems + e) : -1;
+    }
     for (int64_t e0 = warp * 32 * U; e0 < n_entries; e0 += nwarps * 32 * U) {
         int32_t key[U], vtx[U];
         bool tch[U];
         unsigned grp[U];
         int32_t pos[U];
+        int32_t vcur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            vcur[u] = vnext[u];
+            const int64_t en = e0 + nwarps * 32 * U + u * 32 + lane;
+            vnext[u] = en < n_entries ? __ldg(elems + en) : -1;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t e = e0 + u * 32 + lane;
@@ -191,7 +206,7 @@ __global__ void k4_fill(int64_t n_entries, int nv, int32_t n_nodes, int32_t c0, 
             vtx[u] = -1;
             tch[u] = false;
             if (e < n_entries) {
-                const int32_t v = __ldg(elems + e);
+                const int32_t v = vcur[u];
                 // a shard skips the elements that touch none of its columns: no
                 // label gather, no lel row (the column pass never reads it)
                 bool touched = true;
@@ -1224,7 +1239,10 @@ static int v4_fill(fl_ctx* ctx, fl_mesh* mesh, int cap) {
         count_launch(ctx);
     } else if (n_entries > 0) {  // the direct fill (one key per store)
         constexpr int U = 4;
-        const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1), INT_MAX);
+        int per_sm = 1;  // persistent: one resident wave of blocks, warps stride over the entries
+        FL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_fill<U>, 256, 0));
+        const int fgrid = (int)std::min<int64_t>(std::max<int64_t>(div_up(n_entries, 256 * U), 1),
+                                                 (int64_t)ctx->sm_count * std::max(per_sm, 1));
         k4_fill<U><<<fgrid, 256, 0, s>>>(n_entries, nv, N, c0, c1, cap, mesh->elems.as<int32_t>(),
                                          lp.lab.as<int32_t>(), cnt, lp.linc.as<uint32_t>(), lp.lel.as<int32_t>(),
                                          misc);
