@@ -80,10 +80,12 @@ struct ColParams {
     unsigned long long* ov_alloc;  // [2] running A / A(free,free) overflow-staging tops
     const double* nadd;  // Neumann shares per owned column (k_neumann_add), nullptr = none
     bool keys_sorted;    // the plan's segments are already in (j, t) order: no in-kernel sort
-    // label-space pipeline (v4, fl_columns4.cu): columns are labels; inc_ptr / inc
-    // are the label plan's; lel = elements with vertex labels; xl[label] = the
-    // node's coordinates and {node id, free rank or -1} in .w; vst[label] =
-    // {b, u0, b - A u0, 0}
+    // label-space pipeline (v4, fl_columns4.cu): columns are labels; inc holds the
+    // label plan's keys; lel = elements with vertex labels (4 per row); xl[label] =
+    // the node's coordinates and {node id, free rank or -1} in .w; vst[node] =
+    // {b, u0, b - A u0, entry counts}; staging there: st_a_row = the columns' first
+    // kStageFirst 16-byte entries at the node id, st_a_val = their overflow runs,
+    // tile_cap = entries per column
     const int32_t* lel;
     Recip r3, r6;         // recip(3.0), recip(6.0) computed once per context (kernel parameters
                           // are constant-bank operands: no registers held across the column loop)
