@@ -1135,42 +1135,61 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
         if ((int64_t)d0 + total_w > p.cap_a) continue;  // flagged above
         const int cfree_l = fr >= 0 ? 1 : 0;
         int carry_k = -1, carry = 0;
-        for (int32_t q0 = 0; q0 < total_w; q0 += 32) {
-            const int32_t qq = q0 + lane;
-            // largest kk with ex[kk] <= qq (lanes with len 0 share prefixes: the search
-            // lands on the last of them, whose run holds qq)
-            int kk = 0;
+        // two rounds of 32 entries per iteration: both rounds' loads are issued
+        // before either is stored (the copy is bound by bytes in flight)
+        for (int32_t q0 = 0; q0 < total_w; q0 += 64) {
+            int kkv[2];
+            int32_t ekv[2], pfkv[2];
+            int cfv2[2];
+            double2 rec[2];
 #pragma unroll
-            for (int stp = 16; stp > 0; stp >>= 1) {
-                const int32_t ek = __shfl_sync(kFull, ex, kk + stp);
-                if (ek <= qq) kk += stp;
+            for (int r = 0; r < 2; ++r) {
+                const int32_t qq = q0 + 32 * r + lane;
+                // largest kk with ex[kk] <= qq (lanes with len 0 share prefixes: the search
+                // lands on the last of them, whose run holds qq)
+                int kk = 0;
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1) {
+                    const int32_t ek = __shfl_sync(kFull, ex, kk + stp);
+                    if (ek <= qq) kk += stp;
+                }
+                kkv[r] = kk;
+                ekv[r] = __shfl_sync(kFull, ex, kk);
+                const int64_t sk = __shfl_sync(kFull, v, kk);  // the column whose staged run holds qq
+                pfkv[r] = __shfl_sync(kFull, pf, kk);
+                cfv2[r] = __shfl_sync(kFull, cfree_l, kk);
+                rec[r] = make_double2(0.0, 0.0);
+                if (qq < total_w) rec[r] = __ldcs(stage_slot(p, sk, qq - ekv[r]));  // {row | free rank << 32, value}
             }
-            const int32_t ek = __shfl_sync(kFull, ex, kk);
-            const int64_t sk = __shfl_sync(kFull, v, kk);  // the column whose staged run holds qq
-            const int32_t pfk = __shfl_sync(kFull, pf, kk);
-            const int cfree = __shfl_sync(kFull, cfree_l, kk);
-            int2 rf = make_int2(0, -1);
-            double val = 0.0;
-            if (qq < total_w) {
-                const double2 rec = __ldcs(stage_slot(p, sk, qq - ek));  // {row | free rank << 32, value}
-                rf = make_int2(__double2loint(rec.x), __double2hiint(rec.x));
-                val = rec.y;
-                p.row_idx[d0 + qq] = rf.x;
-                p.values[d0 + qq] = val;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int32_t qr = q0 + 32 * r;
+                if (qr >= total_w) break;  // warp-uniform
+                const int32_t qq = qr + lane;
+                const int kk = kkv[r];
+                const int32_t ek = ekv[r];
+                int2 rf = make_int2(0, -1);
+                double val = 0.0;
+                if (qq < total_w) {
+                    rf = make_int2(__double2loint(rec[r].x), __double2hiint(rec[r].x));
+                    val = rec[r].y;
+                    p.row_idx[d0 + qq] = rf.x;
+                    p.values[d0 + qq] = val;
+                }
+                const bool isf = qq < total_w && p.want_sys && cfv2[r] && rf.y >= 0;
+                const unsigned bal = __ballot_sync(kFull, isf);
+                const int start = ek > qr ? (int)(ek - qr) : 0;  // column kk's first lane in this round
+                const unsigned below = (1u << lane) - 1, before = (1u << start) - 1;
+                const int rank = __popc(bal & below & ~before) + (kk == carry_k ? carry : 0);
+                if (isf) {
+                    p.ff_row_idx[pfkv[r] + rank] = rf.y;
+                    p.ff_values[pfkv[r] + rank] = val;
+                }
+                // the column holding lane 31 may continue into the next round
+                const int k31 = __shfl_sync(kFull, kk, 31), st31 = __shfl_sync(kFull, start, 31);
+                carry = (k31 == carry_k ? carry : 0) + __popc(bal & ~((1u << st31) - 1));
+                carry_k = k31;
             }
-            const bool isf = qq < total_w && p.want_sys && cfree && rf.y >= 0;
-            const unsigned bal = __ballot_sync(kFull, isf);
-            const int start = ek > q0 ? (int)(ek - q0) : 0;  // column kk's first lane in this round
-            const unsigned below = (1u << lane) - 1, before = (1u << start) - 1;
-            const int rank = __popc(bal & below & ~before) + (kk == carry_k ? carry : 0);
-            if (isf) {
-                p.ff_row_idx[pfk + rank] = rf.y;
-                p.ff_values[pfk + rank] = val;
-            }
-            // the column holding lane 31 may continue into the next round
-            const int k31 = __shfl_sync(kFull, kk, 31), st31 = __shfl_sync(kFull, start, 31);
-            carry = (k31 == carry_k ? carry : 0) + __popc(bal & ~((1u << st31) - 1));
-            carry_k = k31;
         }
     }
 }
