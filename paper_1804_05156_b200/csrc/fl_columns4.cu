@@ -1051,7 +1051,7 @@ __global__ void __launch_bounds__(V4<D, L, K>::WARPS * 32, MINB) k_columns4(ColP
 // 64 bits: with 256-node tiles a third of the kernel's stalls were blocks waiting
 // for their predecessor); a warp's 32 consecutive columns are one contiguous
 // destination run, copied with every store instruction writing 32 consecutive entries.
-constexpr int kPlaceThreads = 256, kPlaceItems = 4;
+constexpr int kPlaceThreads = 256, kPlaceItems = 4, kPlaceRounds = 4;
 
 __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t* __restrict__ status,
                                                           unsigned int* __restrict__ ticket) {
@@ -1135,15 +1135,16 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
         if ((int64_t)d0 + total_w > p.cap_a) continue;  // flagged above
         const int cfree_l = fr >= 0 ? 1 : 0;
         int carry_k = -1, carry = 0;
-        // two rounds of 32 entries per iteration: both rounds' loads are issued
-        // before either is stored (the copy is bound by bytes in flight)
-        for (int32_t q0 = 0; q0 < total_w; q0 += 64) {
-            int kkv[2];
-            int32_t ekv[2], pfkv[2];
-            int cfv2[2];
-            double2 rec[2];
+        // kPlaceRounds rounds of 32 entries per iteration: all their loads are issued
+        // before any is stored (the copy is bound by bytes in flight; C5 placement
+        // 1.54 / 1.46 / 1.38 ms at 1 / 2 / 4 rounds)
+        for (int32_t q0 = 0; q0 < total_w; q0 += 32 * kPlaceRounds) {
+            int kkv[kPlaceRounds];
+            int32_t ekv[kPlaceRounds], pfkv[kPlaceRounds];
+            int cfv2[kPlaceRounds];
+            double2 rec[kPlaceRounds];
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < kPlaceRounds; ++r) {
                 const int32_t qq = q0 + 32 * r + lane;
                 // largest kk with ex[kk] <= qq (lanes with len 0 share prefixes: the search
                 // lands on the last of them, whose run holds qq)
@@ -1162,7 +1163,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k4_place(ColParams p, uint64_t*
                 if (qq < total_w) rec[r] = __ldcs(stage_slot(p, sk, qq - ekv[r]));  // {row | free rank << 32, value}
             }
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < kPlaceRounds; ++r) {
                 const int32_t qr = q0 + 32 * r;
                 if (qr >= total_w) break;  // warp-uniform
                 const int32_t qq = qr + lane;
